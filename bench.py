@@ -1,0 +1,271 @@
+#!/usr/bin/env python
+"""Benchmark: words/sec of the HogBatch SGNS step on BASELINE.json cfg3 (V=1M, D=300, 800M
+planted Zipf(1.07) tokens, window=5, K=5, t=1e-4), 1..8 B200s, plus its gather/scatter HBM
+roofline fraction.
+
+A step = one `w2v_train(corpus, n, 1)` call = every SURVEY.md §8(a) row over the whole corpus
+(setup a0, subsampling/window a1, sampler a2, fused step a3-a7, L2 window a8, and with N>1 the
+model averaging a9 every 2^20 words per GPU). `value` is device-timed (CUDA events on the
+library's stream, max over ranks) with the corpus resident in HBM; `e2e` is the same call with a
+pinned HOST corpus (H2D inside the timed region). `--impl reference` times the CPU oracle.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import inputs  # noqa: E402
+
+METRIC = "words/sec (1/2/4/8 B200) and fraction of gather/scatter HBM roofline"
+CFG = 3
+SYNC_P = 1 << 20
+REF_SAMPLE = 1 << 17      # raw words per reference step (bounded CPU sample of cfg3)
+BASE_SAMPLE = 1 << 19     # raw words for the cpu_baseline leg
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 7 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 7 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 7 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(cfg, sample):
+    """The oracle as it stands (fp64 sequential O-HB, one host core) on the first `sample` raw
+    words of the workload; setup (counts, tables, init) excluded from the timing."""
+    import oracle
+    ids = cfg.corpus().tokens(0, sample)
+    c = oracle.counts(ids, cfg.V)
+    thr, P = oracle.thresholds(c, sample, cfg.t), oracle.sampler(c)
+    mi, mo = oracle.init(cfg.V, cfg.D, cfg.seed)
+    M_in, M_out = mi.astype(np.float64), mo.astype(np.float64)
+    del mi, mo
+    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, sample)
+    st = oracle.OrcStats()
+    t0 = time.perf_counter()
+    oracle.train_range(prm, thr, P, ids, 0, 0, sample, 0, 0, (sample + cfg.L - 1) // cfg.L, M_in, M_out, st)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": "words/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {sample} raw words of cfg3 (V=1M, D=300), fp64 sequential O-HB, setup excluded",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = inputs.CONFIGS[CFG]
+    import oracle
+    ids = cfg.corpus().tokens(0, REF_SAMPLE)
+    c = oracle.counts(ids, cfg.V)
+    thr, P = oracle.thresholds(c, REF_SAMPLE, cfg.t), oracle.sampler(c)
+    mi, mo = oracle.init(cfg.V, cfg.D, cfg.seed)
+    M_in, M_out = mi.astype(np.float64), mo.astype(np.float64)
+    del mi, mo
+    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, REF_SAMPLE)
+    nch = (REF_SAMPLE + cfg.L - 1) // cfg.L
+    for _ in range(args.warmup):
+        oracle.train_range(prm, thr, P, ids, 0, 0, REF_SAMPLE, 0, 0, nch, M_in, M_out, oracle.OrcStats())
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.train_range(prm, thr, P, ids, 0, 0, REF_SAMPLE, 0, 0, nch, M_in, M_out, oracle.OrcStats())
+    dt = time.perf_counter() - t0
+    v = REF_SAMPLE * args.steps / dt
+    sample = f"first {REF_SAMPLE} raw words of cfg3 per step, fp64 sequential oracle (O-HB), 1 host core"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "words/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 (bounded CPU sample)", "V": cfg.V, "D": cfg.D, "window": cfg.window,
+                   "K": cfg.K, "t": cfg.t, "sample_words": REF_SAMPLE},
+        "cpu_baseline": {"value": v, "unit": "words/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "words/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_06172_b200 import binding as w2v
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = inputs.CONFIGS[CFG]
+    n = cfg.n
+    start, end = w2v.dist_shard(n, cfg.L, world, rank)
+    n_local = end - start
+    host = torch.empty(max(n_local, 1), dtype=torch.int32, pin_memory=True)
+    cfg.corpus().tokens(start, n_local, out=host.numpy())
+    dev = host.cuda()
+    torch.cuda.synchronize()
+
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("sentence_len", cfg.L)
+    w2v.set_option("sync_period_words", SYNC_P)
+    stream = torch.cuda.current_stream()
+    w2v.set_stream(stream.cuda_stream)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(w2v.dist_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        w2v.dist_init(rank, world, bytes(uid.cpu().numpy().tolist()))
+    else:
+        w2v.dist_init(0, 1, None)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        w2v.train(dev, n_local, 1)
+    barrier()
+    steps = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            w2v.train(dev, n_local, 1)
+            steps.append(w2v.get_stats())
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    ms_step_kernel = sum(s["ms_step"] for s in steps) / len(steps)
+    t = torch.tensor([ms, ms_step_kernel], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, kern_max = float(t[0]), float(t[1])
+    value = n * args.steps / (ms_max / 1e3)
+
+    # e2e: the same call with a pinned HOST corpus (H2D + stats D2H inside the timed region)
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        w2v.train(host, n_local, 1)
+    f1.record(stream)
+    barrier()
+    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * e2e_steps / (float(te[0]) / 1e3)
+    last = steps[-1]
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        achieved = last["bytes_row"] / (last["ms_step"] / 1e3) / 1e9   # GB/s, algorithmic bytes
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        out = {
+            "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg3: V=1,000,000 D=300 window=5 K=5 t=1e-4 alpha=0.025, 800M planted "
+                                   "Zipf(1.07) tokens (C=10,000, L=20), 1 epoch per step",
+                       "V": cfg.V, "D": cfg.D, "n_tokens": n, "sync_period_words": SYNC_P if world > 1 else None,
+                       "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
+                       "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
+                       "mode": "hogwild"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "hogbatch_step",
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
+                         "row_bytes_per_word": last["bytes_row"] / n_local,
+                         "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)},
+            "e2e": {"value": e2e_value, "unit": "words/s", "h2d_bytes_per_step": n_local * 4,
+                    "d2h_bytes_per_step": 64},
+            "gpu_launches": int(sum(s["launches"] for s in steps)),
+            "clocks": clk.summary(),
+            "stats": {"loss_per_pair": last["loss_sum"] / max(last["loss_pairs"], 1),
+                      "ms_setup": last["ms_setup"], "ms_step": last["ms_step"], "ms_sync": last["ms_sync"],
+                      "syncs": last["syncs"]},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, BASE_SAMPLE)
+        print(json.dumps(out))
+    w2v.finalize()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,134 @@
+/*
+ * w2v.h — C-ABI of libw2v.so, the B200-native HogBatch skip-gram negative-sampling SGD step
+ * (arXiv 1611.06172). Citations: PAPER.md:L = /root/reference/PAPER.md line L; "Alg.1 l.k" =
+ * PAPER.md line 38+k; C1..C13 and R1..R18 are the contract and readings in DESIGN.md §2-§3.
+ *
+ * Conventions for every call:
+ *  - Returns int: W2V_OK (0) or a negative W2V_E* code; w2v_last_error() then describes it
+ *    (thread-local string, valid until the next call on that thread).
+ *  - One process-global context = one model on the CUDA device current at w2v_init.
+ *  - Pointers marked "host or device" are classified with cudaPointerGetAttributes; they are
+ *    read/written during the call only and never retained. The library owns M_in, M_out,
+ *    the sampler tables and all work buffers (cudaMalloc'd in w2v_init / w2v_train, freed in
+ *    w2v_finalize).
+ *  - Model layout in HBM: one buffer of V rows, row w = [M_in[w] | M_out[w]],
+ *    2·D fp32 per row, so the Zipf-hot rows of BOTH matrices form one contiguous prefix.
+ *  - All work is enqueued on the library stream (w2v_set_stream, default: a private stream);
+ *    every call returns after its work has completed (synchronous API).
+ */
+#ifndef W2V_H_
+#define W2V_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define W2V_OK 0
+#define W2V_EINVAL (-1)   /* bad argument, id outside [0,V), unknown option key, P[V]==0    */
+#define W2V_ESTATE (-2)   /* call out of order (e.g. train before init)                      */
+#define W2V_ENOMEM (-3)   /* device allocation failed; message names the requested bytes      */
+#define W2V_ECUDA  (-4)   /* CUDA runtime error                                               */
+#define W2V_ENCCL  (-5)   /* NCCL error or NCCL library not loadable                          */
+
+typedef struct {
+    int64_t words;        /* raw corpus tokens processed (R14: the unit of words/s)           */
+    int64_t targets;      /* trained targets (kept, N > 0)                                     */
+    int64_t row_touches;  /* sum over targets of N + K + 1 (C12)             */
+    int64_t loss_pairs;   /* sum over targets of N * (K + 1)                                   */
+    double  loss_sum;     /* SGNS loss of the pre-update snapshots (C11), fp64 accumulator     */
+    int64_t syncs;        /* model averagings performed (C13)                                  */
+    int64_t launches;     /* kernels launched by the library in the last w2v_train             */
+    double  ms_total;     /* last w2v_train wall time on the stream (CUDA events), ms          */
+    double  ms_step;      /* ... of which inside the fused hogbatch_step launches, ms          */
+    double  ms_setup;     /* ... of which setup (a0: validate, counts, tables), ms             */
+    double  ms_sync;      /* ... of which model averaging (a9), ms                             */
+    double  ms_h2d;       /* ... of which corpus host->device copy (host-pointer calls), ms    */
+    int64_t step_launches;/* hogbatch_step launches in the last w2v_train                      */
+    int64_t bytes_row;    /* algorithmic row bytes of the last w2v_train: row_touches*4D*2      */
+} w2v_stats_t;
+
+/* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").
+ * V vocabulary size (>=1), D embedding width (>=4, D % 4 == 0, D <= 512), window (>=1, the
+ * maximum half-window of C4; N <= 2*window), K shared negatives (0..31; K=0 degenerates to
+ * logistic regression), alpha initial learning rate (>0, C8), subsample t (>=0,
+ * C2; 0 disables), seed (C1 key). Initialises M_in ~ U[-0.5/D, 0.5/D) and M_out = 0 per C9.
+ * Errors: EINVAL on out-of-range arguments or unsupported (D, K),
+ * ENOMEM naming the 2*V*D*4 bytes requested, ESTATE if already initialised. */
+int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float subsample,
+             uint64_t seed);
+
+/* Set an integer option before w2v_train (SURVEY.md §5 "Config / flags"). Keys:
+ *  "mode"                  0 = Hogwild (default), 1 = deterministic
+ *                          (one work unit, targets in corpus order, R17)
+ *  "sentence_len"          chunk length L of C5 (1..4096; default 1000)
+ *  "sync_period_words"     P of C13 (>=1; default 2^20)
+ *  "lr_quantum"            Q of C8 (>=1; default 10000)
+ *  "allow_target_negative" 0/1 (R2; default 0)
+ *  "debug_base","debug_len" record the batch stream (C5-C7) for global positions
+ *                          [base, base+len) during the next w2v_train (len 0 = off)
+ *  "l2_persist"            0/1 persisting-L2 access window over the hot-row prefix (a8; default 1)
+ *  "ctas_per_sm"           0 = occupancy maximum (default), else that many 1-warp CTAs per SM
+ *  "epochs_total"          E used by the alpha schedule when training is split over several
+ *                          w2v_train calls (0 = the epochs argument of each call; default 0)
+ * Unknown key or bad value -> EINVAL. */
+int w2v_set_option(const char* key, int64_t value);
+
+/* Use this CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream) for all
+ * subsequent work; NULL restores the library's private stream. */
+int w2v_set_stream(void* cuda_stream);
+
+/* Train (PAPER.md:116-126 HogBatch; PAPER.md:135-138 Hogwild across work units).
+ * corpus_ids: int32[n_tokens], host or device, ids in [0,V), this rank's contiguous shard of
+ * the global corpus (C13; with world 1 the whole corpus). Runs, per call: id validation and
+ * counts (global over ranks), thresholds, sampler, then `epochs` epochs of subsampling +
+ * window batching + negative sampling + the fused step, syncing every sync_period_words per
+ * rank (C13). Counts/thresholds/sampler come from this call's corpus. Epoch e of this call
+ * uses RNG epoch field e. n_tokens == 0: no-op success, model unchanged.
+ * Errors: EINVAL (id outside [0,V): nothing trained; P[V] == 0; epochs < 1; shard not
+ * chunk-aligned per C13), ESTATE, ENOMEM, ECUDA, ENCCL. */
+int w2v_train(const int32_t* corpus_ids, int64_t n_tokens, int32_t epochs);
+
+/* Collective (all ranks must call): replace M_in and M_out by their elementwise mean over
+ * ranks (R13). World 1: no-op. */
+int w2v_sync(void);
+
+/* Copy M_in (which = 0) or M_out (which = 1) into dst, V x D fp32 row-major, host or device. */
+int w2v_get_embeddings(int32_t which, float* dst);
+
+/* Overwrite M_in (which = 0) or M_out (which = 1) from src, V x D fp32 row-major, host or
+ * device (resume / test setup). */
+int w2v_set_embeddings(int32_t which, const float* src);
+
+/* Statistics of the last w2v_train (counters are cumulative since w2v_init; ms_* and
+ * launches refer to the last call). */
+int w2v_get_stats(w2v_stats_t* out);
+
+/* Copy the batch stream recorded by the last w2v_train for [debug_base, debug_base+debug_len)
+ * (C5-C7): keep u8[len], b u8[len] (0 = not kept), N u8[len] (0 = not trained), ctx
+ * int32[len][2*window] (-1 padded), neg int32[len][max(K,1)] (-1 padded). Host or device;
+ * any pointer may be NULL. ESTATE if nothing was recorded. */
+int w2v_debug_batches(uint8_t* keep, uint8_t* b, uint8_t* N, int32_t* ctx, int32_t* neg);
+
+/* Data-parallel bootstrap (C13). Rank 0 creates a 128-byte NCCL unique id; the caller
+ * broadcasts it (torch.distributed) and every rank calls w2v_dist_init. world == 1 needs no
+ * id (pass NULL) and makes no NCCL call. Requires libnccl.so.2 (dlopen) when world > 1. */
+int w2v_dist_unique_id(uint8_t out[128]);
+int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]);
+
+/* Pure host planner (no device needed): shard of rank r per C13 and its sync intervals.
+ * out[0..1] = [start, end) global raw positions; out[2] = J intervals per epoch; then
+ * out[3+2k], out[4+2k] = chunk range of interval k, for k < min(J, max_out). Returns J. */
+int64_t w2v_dist_plan(int64_t n_global, int32_t L, int32_t world, int32_t rank,
+                      int64_t sync_period_words, int64_t* out, int64_t max_out);
+
+/* Free everything (model, tables, buffers, NCCL communicator). Safe to call twice. */
+int w2v_finalize(void);
+
+const char* w2v_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* W2V_H_ */

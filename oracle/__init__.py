@@ -225,9 +225,11 @@ def make_params(V, D, window, K, alpha0, t, seed, L, epochs, n_global, world=1, 
 def train_range(prm: OrcParams, thr, P, ids, ids_base, shard_start, n_local, e, chunk_lo, chunk_hi,
                 M_in, M_out, stats: OrcStats, dbg: Debug | None = None, prec="f64") -> None:
     ids = np.ascontiguousarray(ids, np.int32)
+    mi = M_in.ctypes.data if M_in is not None else None      # None: batch stream only
+    mo = M_out.ctypes.data if M_out is not None else None
     rc = lib(prec).orc_train_range(ctypes.byref(prm), _p(thr, ctypes.c_uint64), _p(P, ctypes.c_uint64),
                                    _p(ids, ctypes.c_int32), ids_base, ids.size, shard_start, n_local, e,
-                                   chunk_lo, chunk_hi, M_in.ctypes.data, M_out.ctypes.data, ctypes.byref(stats),
+                                   chunk_lo, chunk_hi, mi, mo, ctypes.byref(stats),
                                    ctypes.byref(dbg.c) if dbg is not None else None)
     if rc != 0:
         raise ValueError("orc_train_range: bad arguments")
@@ -261,3 +263,21 @@ def train(ids, V, D, window, K, alpha0, t, seed, L, epochs=1, prec="f64", lr_qua
     for e in range(epochs):
         train_range(prm, thr, P, ids, 0, 0, n, e, 0, nchunks, M_in, M_out, st, dbg, prec)
     return M_in, M_out, st.as_dict(), dbg
+
+
+def batches(ids, V, window, K, t, seed, L, debug, epoch=0, allow_target_negative=False, counts_global=None,
+            ids_base=0, n_global=None):
+    """Batch stream only (rows a1/a2: keep, b, ctx, negatives) for global positions `debug` =
+    (base, len), without running the SGD step. `ids` holds positions [ids_base, ids_base+len);
+    thresholds and sampler come from `counts_global` (default: counts of `ids`)."""
+    ids = np.ascontiguousarray(ids, np.int32)
+    n = ids.size if n_global is None else n_global
+    c = counts(ids, V) if counts_global is None else counts_global
+    thr, P = thresholds(c, n, t), sampler(c)
+    prm = make_params(V, 4, window, K, 0.025, t, seed, L, 1, n, 1, 10_000, allow_target_negative, 0)
+    dbg = Debug(debug[0], debug[1], window, K)
+    st = OrcStats()
+    lo = debug[0] // L
+    hi = (debug[0] + debug[1] + L - 1) // L
+    train_range(prm, thr, P, ids, ids_base, 0, n, epoch, lo, hi, None, None, st, dbg)
+    return dbg

@@ -363,7 +363,8 @@ int orc_train_range(const orc_params* prm, const uint64_t* thr, const uint64_t* 
                 for (int32_t k = 1; k <= K; ++k)
                     outs[k] = orc_draw_negative(prm->seed, (uint32_t)e, (uint64_t)p, &d, P, V, tw,
                                                 prm->allow_target_negative);
-                loss = orc_hogbatch_step(M_in, M_out, D, ctx, N, outs, K, alpha);
+                /* M_in == NULL: batch stream only (a1/a2 rows), no SGD step */
+                loss = M_in ? orc_hogbatch_step(M_in, M_out, D, ctx, N, outs, K, alpha) : 0.0;
                 st->row_touches += N + K + 1;
             } else {
                 /* O-A1: per-input negatives on the A1NEG stream, idx = i<<12 | (d>>1) */
@@ -385,7 +386,7 @@ int orc_train_range(const orc_params* prm, const uint64_t* thr, const uint64_t* 
                         negs[i * K + (k - 1)] = x;
                     }
                 }
-                loss = orc_alg1_step(M_in, M_out, D, ctx, N, tw, negs, K, alpha);
+                loss = M_in ? orc_alg1_step(M_in, M_out, D, ctx, N, tw, negs, K, alpha) : 0.0;
                 st->row_touches += (int64_t)N * (K + 1) + N;
             }
             st->loss_sum += loss;

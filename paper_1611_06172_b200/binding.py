@@ -1,0 +1,147 @@
+"""Thin ctypes binding of libw2v.so (include/w2v.h). Argument marshalling only: every step of
+the path runs in the library's CUDA kernels. Same names as the C-ABI, minus the `w2v_` prefix.
+
+Arrays may be numpy arrays (host) or torch tensors (host or CUDA); pointers are passed as-is
+and the library classifies them. There is no CPU fallback: if libw2v.so is missing this module
+raises at import.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libw2v.so")
+if not os.path.exists(_SO):
+    raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+_lib = ctypes.CDLL(_SO)
+
+OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("words", ctypes.c_int64), ("targets", ctypes.c_int64), ("row_touches", ctypes.c_int64),
+                ("loss_pairs", ctypes.c_int64), ("loss_sum", ctypes.c_double), ("syncs", ctypes.c_int64),
+                ("launches", ctypes.c_int64), ("ms_total", ctypes.c_double), ("ms_step", ctypes.c_double),
+                ("ms_setup", ctypes.c_double), ("ms_sync", ctypes.c_double), ("ms_h2d", ctypes.c_double),
+                ("step_launches", ctypes.c_int64), ("bytes_row", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_vp = ctypes.c_void_p
+_lib.w2v_init.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_float,
+                          ctypes.c_float, ctypes.c_uint64]
+_lib.w2v_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int64]
+_lib.w2v_set_stream.argtypes = [_vp]
+_lib.w2v_train.argtypes = [_vp, ctypes.c_int64, ctypes.c_int32]
+_lib.w2v_sync.argtypes = []
+_lib.w2v_get_embeddings.argtypes = [ctypes.c_int32, _vp]
+_lib.w2v_set_embeddings.argtypes = [ctypes.c_int32, _vp]
+_lib.w2v_get_stats.argtypes = [ctypes.POINTER(Stats)]
+_lib.w2v_debug_batches.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.w2v_dist_unique_id.argtypes = [_vp]
+_lib.w2v_dist_init.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp]
+_lib.w2v_dist_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                               ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]
+_lib.w2v_dist_plan.restype = ctypes.c_int64
+_lib.w2v_finalize.argtypes = []
+_lib.w2v_last_error.restype = ctypes.c_char_p
+
+
+class W2VError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"w2v error {code}: {msg}")
+        self.code = code
+
+
+def _check(rc):
+    if rc < 0:
+        raise W2VError(rc, _lib.w2v_last_error().decode())
+    return rc
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):          # torch.Tensor (host or device)
+        assert a.is_contiguous()
+        return a.data_ptr()
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous
+    return a.ctypes.data
+
+
+def library_path() -> str:
+    return _SO
+
+
+def init(V, D, window, K, alpha, subsample, seed):
+    return _check(_lib.w2v_init(V, D, window, K, alpha, subsample, seed))
+
+
+def set_option(key: str, value: int):
+    return _check(_lib.w2v_set_option(key.encode(), int(value)))
+
+
+def set_stream(stream_handle):
+    return _check(_lib.w2v_set_stream(stream_handle))
+
+
+def train(corpus_ids, n_tokens=None, epochs=1):
+    n = int(corpus_ids.numel() if hasattr(corpus_ids, "numel") else corpus_ids.size) if n_tokens is None else n_tokens
+    return _check(_lib.w2v_train(_ptr(corpus_ids), n, epochs))
+
+
+def sync():
+    return _check(_lib.w2v_sync())
+
+
+def get_embeddings(which, dst):
+    return _check(_lib.w2v_get_embeddings(which, _ptr(dst)))
+
+
+def set_embeddings(which, src):
+    return _check(_lib.w2v_set_embeddings(which, _ptr(src)))
+
+
+def get_stats() -> dict:
+    s = Stats()
+    _check(_lib.w2v_get_stats(ctypes.byref(s)))
+    return s.as_dict()
+
+
+def debug_batches(keep=None, b=None, N=None, ctx=None, neg=None):
+    return _check(_lib.w2v_debug_batches(_ptr(keep), _ptr(b), _ptr(N), _ptr(ctx), _ptr(neg)))
+
+
+def dist_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.w2v_dist_unique_id(ctypes.cast(buf, _vp)))
+    return bytes(buf)
+
+
+def dist_init(rank, world, uid: bytes | None):
+    buf = None
+    if uid is not None:
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    return _check(_lib.w2v_dist_init(rank, world, ctypes.cast(buf, _vp) if buf is not None else None))
+
+
+def dist_plan(n_global, L, world, rank, sync_period_words):
+    """[(chunk_lo, chunk_hi), ...] sync intervals of `rank` (C13); pure host code."""
+    cap = 1 << 16
+    out = (ctypes.c_int64 * (3 + 2 * cap))()
+    J = _check(_lib.w2v_dist_plan(n_global, L, world, rank, sync_period_words, out, cap))
+    return [(out[3 + 2 * k], out[4 + 2 * k]) for k in range(min(J, cap))]
+
+
+def dist_shard(n_global, L, world, rank):
+    out = (ctypes.c_int64 * 3)()
+    _check(_lib.w2v_dist_plan(n_global, L, world, rank, 1 << 62, out, 0))
+    return out[0], out[1]
+
+
+def finalize():
+    return _check(_lib.w2v_finalize())

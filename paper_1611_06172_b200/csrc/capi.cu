@@ -1,0 +1,529 @@
+// capi.cu — the C-ABI of include/w2v.h: context, options, training driver (setup → epochs →
+// sync intervals → fused step launches), embeddings I/O, statistics, debug export, and the
+// NCCL data-parallel layer (dlopen'd libnccl.so.2, reading R13, C13).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/w2v.h"
+#include "w2v_internal.h"
+
+using namespace w2v;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess) return fail(W2V_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_));  \
+    } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen) ----------
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+    bool load() {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) return false;
+        getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+        commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+        commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+        return getUniqueId && commInitRank && allReduce && commDestroy && getErrorString;
+    }
+} g_nccl;
+
+#define NC(expr)                                                                                         \
+    do {                                                                                                 \
+        ncclResult_t r_ = (expr);                                                                        \
+        if (r_ != ncclSuccess) return fail(W2V_ENCCL, "%s: %s", #expr, g_nccl.getErrorString(r_));      \
+    } while (0)
+
+// ------------------------------------------------------------------ context ----------------
+struct Ctx {
+    bool live = false;
+    int device = 0, sms = 148;
+    int64_t V = 0;
+    int32_t D = 0, window = 0, K = 0;
+    float alpha = 0.f, t = 0.f;
+    uint64_t seed = 0;
+    // options
+    int mode = 0;
+    int32_t L = 1000;
+    int64_t sync_period = 1 << 20;
+    int64_t Q = 10000;
+    int allow_tn = 0;
+    int64_t dbg_base = 0, dbg_len = 0;
+    int l2_persist = 1;
+    int ctas_per_sm = 0;
+    int32_t epochs_total = 0;
+    // device state
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    float* M = nullptr;  // V rows of [M_in | M_out]
+    int32_t* corpus = nullptr;
+    size_t corpus_cap = 0;
+    unsigned long long* counts = nullptr;
+    uint64_t *thr = nullptr, *P = nullptr, *scratch = nullptr;
+    int32_t* G = nullptr;
+    int gbits = 0;
+    SetupInfo* info = nullptr;
+    DevStats* dstats = nullptr;
+    unsigned long long* chunk_ctr = nullptr;
+    int64_t* dp_tmp = nullptr;
+    // debug
+    uint8_t *dbg_keep = nullptr, *dbg_b = nullptr, *dbg_N = nullptr;
+    int32_t *dbg_ctx = nullptr, *dbg_neg = nullptr;
+    int64_t dbg_rec_len = 0;
+    // dist
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    // stats
+    w2v_stats_t st{};
+} g;
+
+void free_dbg() {
+    cudaFree(g.dbg_keep); cudaFree(g.dbg_b); cudaFree(g.dbg_N); cudaFree(g.dbg_ctx); cudaFree(g.dbg_neg);
+    g.dbg_keep = g.dbg_b = g.dbg_N = nullptr;
+    g.dbg_ctx = g.dbg_neg = nullptr;
+    g.dbg_rec_len = 0;
+}
+
+int dmalloc(void** p, size_t bytes, const char* what) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(W2V_ENOMEM, "cudaMalloc of %zu bytes for %s failed: %s", bytes, what, cudaGetErrorString(e));
+    }
+    return W2V_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// C13 host plan
+struct Plan {
+    int64_t S, lo, hi, start, end, J, I;
+};
+Plan make_plan(int64_t n, int32_t L, int32_t W, int32_t r, int64_t P) {
+    Plan p{};
+    p.S = (n + L - 1) / L;
+    p.lo = (int64_t)r * p.S / W;
+    p.hi = ((int64_t)r + 1) * p.S / W;
+    p.start = p.lo * L;
+    p.end = std::min(p.hi * L, n);
+    p.I = std::max<int64_t>(1, P / L);
+    int64_t mins = INT64_MAX;
+    for (int q = 0; q < W; ++q) mins = std::min(mins, ((int64_t)q + 1) * p.S / W - (int64_t)q * p.S / W);
+    p.J = std::max<int64_t>(1, mins / p.I);
+    return p;
+}
+
+int sync_models() {
+    if (g.world <= 1) return W2V_OK;
+    NC(g_nccl.allReduce(g.M, g.M, (size_t)g.V * 2 * g.D, ncclFloat32, ncclAvg, g.comm, g.stream));
+    g.st.syncs += 1;
+    return W2V_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* w2v_last_error(void) { return g_err.c_str(); }
+
+int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float subsample, uint64_t seed) {
+    if (g.live) return fail(W2V_ESTATE, "w2v_init: already initialised (call w2v_finalize first)");
+    if (V < 1 || V > 2147483647ll) return fail(W2V_EINVAL, "w2v_init: V=%lld out of [1, 2^31)", (long long)V);
+    if (D < 4 || D % 4 != 0 || D > 512) return fail(W2V_EINVAL, "w2v_init: D=%d must be a multiple of 4 in [4,512]", D);
+    if (window < 1 || window > 254) return fail(W2V_EINVAL, "w2v_init: window=%d out of [1,254]", window);
+    if (K < 0 || K > 31) return fail(W2V_EINVAL, "w2v_init: K=%d out of [0,31]", K);
+    if (!(alpha > 0.f) || !std::isfinite(alpha)) return fail(W2V_EINVAL, "w2v_init: alpha must be > 0");
+    if (!(subsample >= 0.f) || !std::isfinite(subsample)) return fail(W2V_EINVAL, "w2v_init: subsample must be >= 0");
+    if (!step_supported(D, K)) return fail(W2V_EINVAL, "w2v_init: (D=%d, K=%d) exceeds the register tiles (DESIGN.md §8)", D, K);
+    Ctx fresh;
+    g = fresh;
+    CU(cudaGetDevice(&g.device));
+    CU(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, g.device));
+    g.V = V; g.D = D; g.window = window; g.K = K; g.alpha = alpha; g.t = subsample; g.seed = seed;
+    CU(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
+    g.stream = g.own_stream;
+    int rc;
+    if ((rc = dmalloc((void**)&g.M, (size_t)V * 2 * D * sizeof(float), "the model [M_in|M_out]"))) return rc;
+    if ((rc = dmalloc((void**)&g.counts, (size_t)V * 8, "counts"))) return rc;
+    if ((rc = dmalloc((void**)&g.thr, (size_t)V * 8, "keep thresholds"))) return rc;
+    if ((rc = dmalloc((void**)&g.P, (size_t)(V + 1) * 8, "sampler prefix"))) return rc;
+    const int64_t nb = (V + 2047) / 2048;
+    if ((rc = dmalloc((void**)&g.scratch, (size_t)(nb + 1) * 8, "scan scratch"))) return rc;
+    g.gbits = 1;
+    while ((1ll << g.gbits) < V) ++g.gbits;
+    g.gbits += 1;
+    if ((rc = dmalloc((void**)&g.G, (size_t)((1ll << g.gbits) + 2) * 4, "guide table"))) return rc;
+    if ((rc = dmalloc((void**)&g.info, sizeof(SetupInfo), "setup info"))) return rc;
+    if ((rc = dmalloc((void**)&g.dstats, sizeof(DevStats), "stats"))) return rc;
+    if ((rc = dmalloc((void**)&g.chunk_ctr, 64, "chunk counter"))) return rc;
+    CU(launch_init(g.M, V, D, seed, g.sms, g.stream));
+    CU(cudaStreamSynchronize(g.stream));
+    g.live = true;
+    return W2V_OK;
+}
+
+int w2v_set_option(const char* key, int64_t v) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_set_option before w2v_init");
+    if (!key) return fail(W2V_EINVAL, "w2v_set_option: null key");
+    std::string k(key);
+    if (k == "mode") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "mode must be 0 or 1"); g.mode = (int)v; }
+    else if (k == "sentence_len") { if (v < 1 || v > 4096) return fail(W2V_EINVAL, "sentence_len out of [1,4096]"); g.L = (int32_t)v; }
+    else if (k == "sync_period_words") { if (v < 1) return fail(W2V_EINVAL, "sync_period_words must be >= 1"); g.sync_period = v; }
+    else if (k == "lr_quantum") { if (v < 1) return fail(W2V_EINVAL, "lr_quantum must be >= 1"); g.Q = v; }
+    else if (k == "allow_target_negative") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "allow_target_negative must be 0/1"); g.allow_tn = (int)v; }
+    else if (k == "debug_base") { if (v < 0) return fail(W2V_EINVAL, "debug_base must be >= 0"); g.dbg_base = v; }
+    else if (k == "debug_len") { if (v < 0) return fail(W2V_EINVAL, "debug_len must be >= 0"); g.dbg_len = v; }
+    else if (k == "l2_persist") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "l2_persist must be 0/1"); g.l2_persist = (int)v; }
+    else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
+    else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
+    else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
+    return W2V_OK;
+}
+
+int w2v_set_stream(void* s) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_set_stream before w2v_init");
+    g.stream = s ? (cudaStream_t)s : g.own_stream;
+    return W2V_OK;
+}
+
+int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_train before w2v_init");
+    if (epochs < 1) return fail(W2V_EINVAL, "w2v_train: epochs=%d must be >= 1", epochs);
+    if (n < 0) return fail(W2V_EINVAL, "w2v_train: n_tokens < 0");
+    g.st.launches = 0;
+    g.st.ms_total = g.st.ms_step = g.st.ms_setup = g.st.ms_sync = g.st.ms_h2d = 0;
+    g.st.step_launches = 0;
+    g.st.bytes_row = 0;
+    // the union of the shards may be non-empty while this rank's shard is empty: only a
+    // world-1 empty corpus is a pure no-op
+    if (n == 0 && g.world == 1) return W2V_OK;
+    if (!ids_in && n > 0) return fail(W2V_EINVAL, "w2v_train: null corpus");
+    cudaStream_t st = g.stream;
+    int launches = 0;
+    cudaEvent_t ev0, ev_h2d, ev_setup, ev_end;
+    CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev_h2d)); CU(cudaEventCreate(&ev_setup)); CU(cudaEventCreate(&ev_end));
+    CU(cudaEventRecord(ev0, st));
+    // ---- corpus placement
+    const int32_t* ids = ids_in;
+    if (n > 0 && !is_device_ptr(ids_in)) {
+        if ((size_t)n > g.corpus_cap) {
+            cudaFree(g.corpus);
+            g.corpus = nullptr;
+            g.corpus_cap = 0;
+            int rc = dmalloc((void**)&g.corpus, (size_t)n * 4, "the device copy of a host corpus");
+            if (rc) return rc;
+            g.corpus_cap = (size_t)n;
+        }
+        CU(cudaMemcpyAsync(g.corpus, ids_in, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        ids = g.corpus;
+    }
+    CU(cudaEventRecord(ev_h2d, st));
+    // ---- a0: shard geometry (C13), counts, thresholds, sampler
+    int64_t n_global = n, shard_start = 0;
+    if (g.world > 1) {
+        if (!g.dp_tmp) { int rc = dmalloc((void**)&g.dp_tmp, (size_t)g.world * 8, "dp scratch"); if (rc) return rc; }
+        std::vector<int64_t> h(g.world, 0);
+        h[g.rank] = n;
+        CU(cudaMemcpyAsync(g.dp_tmp, h.data(), (size_t)g.world * 8, cudaMemcpyHostToDevice, st));
+        NC(g_nccl.allReduce(g.dp_tmp, g.dp_tmp, (size_t)g.world, ncclInt64, ncclSum, g.comm, st));
+        CU(cudaMemcpyAsync(h.data(), g.dp_tmp, (size_t)g.world * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        n_global = 0;
+        for (int q = 0; q < g.world; ++q) { if (q < g.rank) shard_start += h[q]; n_global += h[q]; }
+        if (n_global == 0) return W2V_OK;
+        const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
+        if (pl.start != shard_start || pl.end - pl.start != n)
+            return fail(W2V_EINVAL, "w2v_train: rank %d shard [%lld,%lld) is not the C13 shard [%lld,%lld) of n=%lld, L=%d",
+                        g.rank, (long long)shard_start, (long long)(shard_start + n), (long long)pl.start,
+                        (long long)pl.end, (long long)n_global, g.L);
+    }
+    CU(cudaMemsetAsync(g.counts, 0, (size_t)g.V * 8, st));
+    CU(cudaMemsetAsync(g.info, 0, sizeof(SetupInfo), st));
+    CU(launch_hist(ids, n, g.V, g.counts, g.info, g.sms, st, &launches));
+    if (g.world > 1) NC(g_nccl.allReduce(g.counts, g.counts, (size_t)g.V, ncclUint64, ncclSum, g.comm, st));
+    CU(launch_tables(g.counts, g.V, n_global, g.t, g.thr, g.P, g.scratch, g.G, g.gbits, g.info, st, &launches));
+    SetupInfo hinfo{};
+    CU(cudaMemcpyAsync(&hinfo, g.info, sizeof hinfo, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (g.world > 1) {
+        // every rank must take the same exit: combine the bad-id flags
+        std::vector<int64_t> h(g.world, 0);
+        h[g.rank] = hinfo.bad_id;
+        CU(cudaMemcpyAsync(g.dp_tmp, h.data(), (size_t)g.world * 8, cudaMemcpyHostToDevice, st));
+        NC(g_nccl.allReduce(g.dp_tmp, g.dp_tmp, (size_t)g.world, ncclInt64, ncclSum, g.comm, st));
+        CU(cudaMemcpyAsync(h.data(), g.dp_tmp, (size_t)g.world * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        for (int q = 0; q < g.world; ++q) hinfo.bad_id |= (int)h[q];
+    }
+    if (hinfo.bad_id) return fail(W2V_EINVAL, "w2v_train: corpus contains an id outside [0,%lld); nothing trained", (long long)g.V);
+    if (hinfo.PV == 0) return fail(W2V_EINVAL, "w2v_train: sampler mass P[V] is 0");
+    CU(cudaEventRecord(ev_setup, st));
+    // ---- debug buffers
+    free_dbg();
+    if (g.dbg_len > 0) {
+        const int64_t Lq = g.dbg_len, kk = g.K > 0 ? g.K : 1;
+        int rc;
+        if ((rc = dmalloc((void**)&g.dbg_keep, Lq, "debug keep"))) return rc;
+        if ((rc = dmalloc((void**)&g.dbg_b, Lq, "debug b"))) return rc;
+        if ((rc = dmalloc((void**)&g.dbg_N, Lq, "debug N"))) return rc;
+        if ((rc = dmalloc((void**)&g.dbg_ctx, (size_t)Lq * 2 * g.window * 4, "debug ctx"))) return rc;
+        if ((rc = dmalloc((void**)&g.dbg_neg, (size_t)Lq * kk * 4, "debug neg"))) return rc;
+        CU(cudaMemsetAsync(g.dbg_keep, 0, Lq, st));
+        CU(cudaMemsetAsync(g.dbg_b, 0, Lq, st));
+        CU(cudaMemsetAsync(g.dbg_N, 0, Lq, st));
+        CU(cudaMemsetAsync(g.dbg_ctx, 0xff, (size_t)Lq * 2 * g.window * 4, st));
+        CU(cudaMemsetAsync(g.dbg_neg, 0xff, (size_t)Lq * kk * 4, st));
+        g.dbg_rec_len = Lq;
+    }
+    // ---- a8: persisting-L2 window over the hot prefix rows of [M_in|M_out]
+    bool window_set = false;
+    if (g.l2_persist && g.mode == 0) {
+        int maxp = 0, maxwin = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g.device);
+        cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g.device);
+        if (maxp > 0 && maxwin > 0) {
+            size_t bytes = std::min<size_t>((size_t)maxp, (size_t)maxwin);
+            bytes = std::min<size_t>(bytes, (size_t)g.V * 2 * g.D * 4);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess) {
+                cudaStreamAttrValue a{};
+                a.accessPolicyWindow.base_ptr = g.M;
+                a.accessPolicyWindow.num_bytes = bytes;
+                a.accessPolicyWindow.hitRatio = 1.0f;
+                a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                window_set = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess;
+            }
+        }
+        cudaGetLastError();
+    }
+    // ---- epochs × sync intervals of fused steps
+    StepParams p{};
+    p.ids = ids;
+    p.ids_base = shard_start;
+    p.shard_start = shard_start;
+    p.n_local = n;
+    p.n_global = n_global;
+    p.L = g.L; p.window = g.window; p.K = g.K; p.D = g.D;
+    p.epochs = g.epochs_total > 0 ? g.epochs_total : epochs;
+    p.world = g.world;
+    p.allow_tn = g.allow_tn;
+    p.deterministic = g.mode;
+    p.alpha0 = g.alpha; p.Q = g.Q; p.seed = g.seed; p.V = g.V;
+    p.thr = g.thr; p.P = g.P; p.G = g.G; p.info = g.info; p.M = g.M;
+    p.chunk_ctr = g.chunk_ctr; p.stats = g.dstats;
+    p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
+    p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
+    const size_t wb = step_warp_bytes(g.L, g.window, g.K, g.D, &p.slab_offset);
+    if (wb > 227 * 1024) return fail(W2V_EINVAL, "w2v_train: per-warp shared memory %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
+    p.warp_bytes = (int32_t)wb;
+    int ctas = 1;
+    if (g.mode == 0) {
+        int occ = step_max_ctas_per_sm(p);
+        if (occ < 1) return fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per warp)", wb);
+        if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
+        ctas = g.sms * occ;
+    }
+    CU(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
+    const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
+    const int64_t chunk_lo = shard_start / g.L;
+    const int64_t chunk_hi = (shard_start + n + g.L - 1) / g.L;
+    std::vector<cudaEvent_t> evs;
+    std::vector<int> ev_kind;  // 0 step, 1 sync
+    auto mark = [&](int kind) -> cudaError_t {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r != cudaSuccess) return r;
+        evs.push_back(e);
+        ev_kind.push_back(kind);
+        return cudaEventRecord(e, st);
+    };
+    for (int32_t e = 0; e < epochs; ++e) {
+        p.epoch = e;
+        const int64_t J = g.world > 1 ? pl.J : 1;
+        for (int64_t k = 0; k < J; ++k) {
+            p.chunk_lo = g.world > 1 ? chunk_lo + k * pl.I : chunk_lo;
+            p.chunk_hi = (g.world > 1 && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
+            CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
+            CU(mark(0));
+            CU(launch_step(p, ctas, st));
+            ++launches;
+            ++g.st.step_launches;
+            CU(mark(0));
+            if (g.world > 1) {
+                CU(mark(1));
+                int rc = sync_models();
+                if (rc) return rc;
+                CU(mark(1));
+            }
+        }
+    }
+    CU(cudaEventRecord(ev_end, st));
+    DevStats hs{};
+    CU(cudaMemcpyAsync(&hs, g.dstats, sizeof hs, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (window_set) {
+        cudaStreamAttrValue a{};
+        a.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+        cudaCtxResetPersistingL2Cache();
+        cudaGetLastError();
+    }
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, ev0, ev_end)); g.st.ms_total = ms;
+    CU(cudaEventElapsedTime(&ms, ev0, ev_h2d)); g.st.ms_h2d = ms;
+    CU(cudaEventElapsedTime(&ms, ev_h2d, ev_setup)); g.st.ms_setup = ms;
+    for (size_t i = 0; i + 1 < evs.size(); i += 2) {
+        CU(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
+        if (ev_kind[i] == 0) g.st.ms_step += ms; else g.st.ms_sync += ms;
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+    cudaEventDestroy(ev0); cudaEventDestroy(ev_h2d); cudaEventDestroy(ev_setup); cudaEventDestroy(ev_end);
+    g.st.words += (int64_t)hs.words;
+    g.st.targets += (int64_t)hs.targets;
+    g.st.row_touches += (int64_t)hs.row_touches;
+    g.st.loss_pairs += (int64_t)hs.loss_pairs;
+    g.st.loss_sum += hs.loss_sum;
+    g.st.launches = launches;
+    g.st.bytes_row = (int64_t)hs.row_touches * 4 * g.D * 2;
+    return W2V_OK;
+}
+
+int w2v_sync(void) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_sync before w2v_init");
+    int rc = sync_models();
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(g.stream));
+    return W2V_OK;
+}
+
+int w2v_get_embeddings(int32_t which, float* dst) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_get_embeddings before w2v_init");
+    if ((which != 0 && which != 1) || !dst) return fail(W2V_EINVAL, "w2v_get_embeddings: which must be 0/1, dst non-null");
+    const size_t row = (size_t)g.D * 4;
+    CU(cudaMemcpy2DAsync(dst, row, g.M + (which ? g.D : 0), 2 * row, row, (size_t)g.V, cudaMemcpyDefault, g.stream));
+    CU(cudaStreamSynchronize(g.stream));
+    return W2V_OK;
+}
+
+int w2v_set_embeddings(int32_t which, const float* src) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_set_embeddings before w2v_init");
+    if ((which != 0 && which != 1) || !src) return fail(W2V_EINVAL, "w2v_set_embeddings: which must be 0/1, src non-null");
+    const size_t row = (size_t)g.D * 4;
+    CU(cudaMemcpy2DAsync(g.M + (which ? g.D : 0), 2 * row, src, row, row, (size_t)g.V, cudaMemcpyDefault, g.stream));
+    CU(cudaStreamSynchronize(g.stream));
+    return W2V_OK;
+}
+
+int w2v_get_stats(w2v_stats_t* out) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_get_stats before w2v_init");
+    if (!out) return fail(W2V_EINVAL, "w2v_get_stats: null out");
+    *out = g.st;
+    return W2V_OK;
+}
+
+int w2v_debug_batches(uint8_t* keep, uint8_t* b, uint8_t* N, int32_t* ctx, int32_t* neg) {
+    if (!g.live || g.dbg_rec_len == 0) return fail(W2V_ESTATE, "w2v_debug_batches: nothing recorded");
+    const int64_t Lq = g.dbg_rec_len, kk = g.K > 0 ? g.K : 1;
+    if (keep) CU(cudaMemcpyAsync(keep, g.dbg_keep, Lq, cudaMemcpyDefault, g.stream));
+    if (b) CU(cudaMemcpyAsync(b, g.dbg_b, Lq, cudaMemcpyDefault, g.stream));
+    if (N) CU(cudaMemcpyAsync(N, g.dbg_N, Lq, cudaMemcpyDefault, g.stream));
+    if (ctx) CU(cudaMemcpyAsync(ctx, g.dbg_ctx, (size_t)Lq * 2 * g.window * 4, cudaMemcpyDefault, g.stream));
+    if (neg) CU(cudaMemcpyAsync(neg, g.dbg_neg, (size_t)Lq * kk * 4, cudaMemcpyDefault, g.stream));
+    CU(cudaStreamSynchronize(g.stream));
+    return W2V_OK;
+}
+
+int w2v_dist_unique_id(uint8_t out[128]) {
+    if (!out) return fail(W2V_EINVAL, "w2v_dist_unique_id: null out");
+    if (!g_nccl.load()) return fail(W2V_ENCCL, "cannot dlopen libnccl.so.2: %s", dlerror());
+    ncclUniqueId id;
+    NC(g_nccl.getUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return W2V_OK;
+}
+
+int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
+    if (!g.live) return fail(W2V_ESTATE, "w2v_dist_init before w2v_init");
+    if (world < 1 || rank < 0 || rank >= world) return fail(W2V_EINVAL, "w2v_dist_init: rank %d / world %d", rank, world);
+    if (g.comm) return fail(W2V_ESTATE, "w2v_dist_init: already initialised");
+    g.rank = rank;
+    g.world = world;
+    if (world == 1) return W2V_OK;
+    if (!id) return fail(W2V_EINVAL, "w2v_dist_init: null id with world > 1");
+    if (!g_nccl.load()) return fail(W2V_ENCCL, "cannot dlopen libnccl.so.2: %s", dlerror());
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    NC(g_nccl.commInitRank(&g.comm, world, uid, rank));
+    return W2V_OK;
+}
+
+int64_t w2v_dist_plan(int64_t n_global, int32_t L, int32_t world, int32_t rank, int64_t P, int64_t* out,
+                      int64_t max_out) {
+    if (n_global < 0 || L < 1 || world < 1 || rank < 0 || rank >= world || P < 1 || !out)
+        return fail(W2V_EINVAL, "w2v_dist_plan: bad arguments");
+    const Plan pl = make_plan(n_global, L, world, rank, P);
+    out[0] = pl.start;
+    out[1] = pl.end;
+    out[2] = pl.J;
+    for (int64_t k = 0; k < pl.J && k < max_out; ++k) {
+        out[3 + 2 * k] = pl.lo + k * pl.I;
+        out[4 + 2 * k] = (k == pl.J - 1) ? pl.hi : pl.lo + (k + 1) * pl.I;
+    }
+    return pl.J;
+}
+
+int w2v_finalize(void) {
+    if (!g.live) return W2V_OK;
+    cudaStreamSynchronize(g.stream);
+    if (g.comm) g_nccl.commDestroy(g.comm);
+    free_dbg();
+    cudaFree(g.M); cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
+    cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
+    cudaStreamDestroy(g.own_stream);
+    Ctx fresh;
+    g = fresh;
+    return W2V_OK;
+}
+
+}  // extern "C"

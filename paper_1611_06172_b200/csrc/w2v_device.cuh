@@ -1,0 +1,63 @@
+// w2v_device.cuh — device primitives of the CUDA path (sm_100a). Independent of oracle/:
+// written from the contract text, not from the oracle's source.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace w2v {
+
+enum : uint32_t { kTagPos = 1, kTagNeg = 2, kTagInit = 3 };
+
+// C1: Philox4x32-10, key = seed, counter = (p lo, p hi, e, tag<<24 | idx).
+struct U4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ U4 philox(uint64_t seed, uint32_t tag, uint32_t e, uint64_t p, uint32_t idx) {
+    uint32_t c0 = (uint32_t)p, c1 = (uint32_t)(p >> 32), c2 = e, c3 = (tag << 24) | idx;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    return U4{c0, c1, c2, c3};
+}
+
+// C3: smallest w in [lo, hi] with P[w+1] > x (predicate monotone in w; answer known in range)
+__device__ __forceinline__ int64_t invcdf_range(const uint64_t* __restrict__ P, int64_t lo, int64_t hi,
+                                                uint64_t x) {
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (__ldg(P + mid + 1) > x) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// C3 accelerated by the guide table: G[k] = invcdf(min(k << gshift, P[V]-1)).
+__device__ __forceinline__ int32_t invcdf_guided(const uint64_t* __restrict__ P, const int32_t* __restrict__ G,
+                                                 int gshift, uint64_t x) {
+    const uint64_t k = x >> gshift;
+    return (int32_t)invcdf_range(P, __ldg(G + k), __ldg(G + k + 1), x);
+}
+
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// Hogwild scatter: vector reduction at L2, no lost updates, no return (sm_90+ red.v4.f32).
+__device__ __forceinline__ void red_add_v4(float* gaddr, float4 v) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(gaddr), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+// 16-byte async global->shared copy, L2 only (cp.async.cg, LDGSTS.BYPASS)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ float softplus_f(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
+
+}  // namespace w2v

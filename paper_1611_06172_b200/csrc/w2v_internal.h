@@ -1,0 +1,61 @@
+// w2v_internal.h — structures shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace w2v {
+
+// Written by the setup kernels, read by the step kernel and (once per w2v_train) by the host.
+struct SetupInfo {
+    uint64_t PV;       // P[V], total sampler mass (C3)
+    int32_t gshift;    // guide-table bucket shift
+    int32_t bad_id;    // 1 if an id outside [0,V) was seen
+    int64_t first_bad; // (unused by kernels; host diagnostics)
+};
+
+struct DevStats {
+    unsigned long long words, targets, row_touches, loss_pairs;
+    double loss_sum;
+};
+
+struct StepParams {
+    const int32_t* ids;   // ids[k] = token at global position ids_base + k
+    int64_t ids_base;
+    int64_t shard_start, n_local, n_global;
+    int64_t chunk_lo, chunk_hi;  // global chunk range of this launch
+    int32_t L, window, K, D;
+    int32_t epoch, epochs, world;
+    int32_t allow_tn, deterministic;
+    float alpha0;
+    int64_t Q;
+    uint64_t seed;
+    int64_t V;
+    const uint64_t* thr;
+    const uint64_t* P;
+    const int32_t* G;
+    const SetupInfo* info;
+    float* M;  // interleaved model: row w = [M_in[w] (D) | M_out[w] (D)]
+    unsigned long long* chunk_ctr;
+    DevStats* stats;
+    int64_t dbg_base, dbg_len;
+    uint8_t *dbg_keep, *dbg_b, *dbg_N;
+    int32_t *dbg_ctx, *dbg_neg;
+    int32_t warp_bytes;   // dynamic shared memory per warp
+    int32_t slab_offset;  // byte offset of the row slab inside a warp's region
+};
+
+// setup.cu
+cudaError_t launch_hist(const int32_t* ids, int64_t n, int64_t V, unsigned long long* counts, SetupInfo* info,
+                        int sms, cudaStream_t st, int* launches);
+cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T, float t, uint64_t* thr,
+                          uint64_t* P, uint64_t* scratch, int32_t* G, int gbits, SetupInfo* info, cudaStream_t st,
+                          int* launches);
+cudaError_t launch_init(float* M, int64_t V, int32_t D, uint64_t seed, int sms, cudaStream_t st);
+
+// hogbatch.cu
+bool step_supported(int D, int K);
+cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st);
+int step_max_ctas_per_sm(const StepParams& p);
+size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
+
+}  // namespace w2v

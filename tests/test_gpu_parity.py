@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Bars: batch stream (keep flags, b, context ids, negatives), counts-derived
+statistics and the init are BIT-EXACT; deterministic-mode embeddings within 1e-5 relative L2 of
+the fp64 oracle; Hogwild-mode loss within 1% and planted-cluster recall within 0.02.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def w2v():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    from paper_1611_06172_b200 import binding
+    torch.cuda.set_device(0)
+    binding.finalize()
+    yield binding
+    binding.finalize()
+
+
+def rel_l2(a, ref):
+    a = np.asarray(a, np.float64); ref = np.asarray(ref, np.float64)
+    return float(np.linalg.norm(a - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+def run_gpu(w2v, ids, V, D, window, K, alpha, t, seed, L, epochs=1, mode=1, debug=None, opts=None, device=True,
+            model=None):
+    w2v.init(V, D, window, K, alpha, t, seed)
+    w2v.set_option("mode", mode)
+    w2v.set_option("sentence_len", L)
+    for k, v in (opts or {}).items():
+        w2v.set_option(k, v)
+    if model is not None:
+        w2v.set_embeddings(0, np.ascontiguousarray(model[0], np.float32))
+        w2v.set_embeddings(1, np.ascontiguousarray(model[1], np.float32))
+    if debug:
+        w2v.set_option("debug_base", debug[0])
+        w2v.set_option("debug_len", debug[1])
+    src = torch.from_numpy(np.ascontiguousarray(ids, np.int32))
+    if device:
+        src = src.cuda()
+    w2v.train(src, ids.size, epochs)
+    M_in = np.empty((V, D), np.float32); M_out = np.empty((V, D), np.float32)
+    w2v.get_embeddings(0, M_in); w2v.get_embeddings(1, M_out)
+    out = {"M_in": M_in, "M_out": M_out, "stats": w2v.get_stats()}
+    if debug:
+        n = debug[1]
+        d = {"keep": np.zeros(n, np.uint8), "b": np.zeros(n, np.uint8), "N": np.zeros(n, np.uint8),
+             "ctx": np.zeros((n, 2 * window), np.int32), "neg": np.zeros((n, max(K, 1)), np.int32)}
+        w2v.debug_batches(d["keep"], d["b"], d["N"], d["ctx"], d["neg"])
+        out["dbg"] = d
+    return out
+
+
+def assert_stream_equal(gdbg, odbg):
+    for f in ("keep", "b", "N", "ctx", "neg"):
+        assert np.array_equal(gdbg[f], getattr(odbg, f)), f"{f}: {np.argwhere(gdbg[f] != getattr(odbg, f))[:5]}"
+
+
+# ------------------------------------------------------------------ init (C9) ----------------
+def test_init_bitexact(w2v):
+    for V, D, seed in [(1000, 32, 1001), (777, 300, 5), (3, 4, 0)]:
+        w2v.init(V, D, 2, 3, 0.025, 0.0, seed)
+        M_in = np.empty((V, D), np.float32); M_out = np.empty((V, D), np.float32)
+        w2v.get_embeddings(0, M_in); w2v.get_embeddings(1, M_out)
+        w2v.finalize()
+        o_in, o_out = oracle.init(V, D, seed)
+        assert np.array_equal(M_in.view(np.uint32), o_in.view(np.uint32))
+        assert np.all(M_out == 0)
+
+
+# ------------------------------------------------------------------ cfg1 parity --------------
+@pytest.mark.parametrize("n", [1000, 5000, 20000])
+def test_cfg1_deterministic_parity(w2v, n):
+    """BASELINE cfg1 (V=1000, D=32, window=2, K=3, t=0, Zipf(1.0)): bit-exact batch stream and
+    <=1e-5 relative L2 of both matrices against the fp64 oracle after n raw tokens."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, n)
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, n))
+    o_in, o_out, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                            debug=(0, n))
+    assert_stream_equal(g["dbg"], o_dbg)
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert g["stats"][k] == o_st[k], k
+    assert abs(g["stats"]["loss_sum"] - o_st["loss_sum"]) <= 1e-5 * abs(o_st["loss_sum"])
+    f_in, f_out, _, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                     prec="f32")
+    e_in, e_out = rel_l2(g["M_in"], o_in), rel_l2(g["M_out"], o_out)
+    print(f"n={n}: GPU vs fp64 oracle rel L2 M_in {e_in:.2e} M_out {e_out:.2e}; "
+          f"fp32 oracle vs fp64: {rel_l2(f_in, o_in):.2e} {rel_l2(f_out, o_out):.2e}")
+    assert e_in <= 1e-5 and e_out <= 1e-5
+
+
+def test_cfg1_hogwild_stream_and_loss(w2v):
+    """Hogwild mode (persistent grid, all SMs) on cfg1: the batch stream does not depend on the
+    model, so it stays bit-exact; loss within 1% of the oracle's."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, cfg.n)
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, mode=0,
+                debug=(0, cfg.n))
+    _, _, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                     debug=(0, cfg.n))
+    assert_stream_equal(g["dbg"], o_dbg)
+    assert g["stats"]["row_touches"] == o_st["row_touches"]
+    assert abs(g["stats"]["loss_sum"] / o_st["loss_sum"] - 1) < 0.01
+
+
+# ------------------------------------------------------------------ edge cases ---------------
+@pytest.mark.parametrize("V,D,window,K,t,L,n,epochs,allow", [
+    (50, 4, 1, 0, 0.0, 7, 333, 1, 0),          # K=0 (logistic regression), tiny D, ragged chunks
+    (200, 36, 3, 5, 1e-2, 64, 5_001, 2, 0),    # D not a multiple of 32, 2 epochs, subsampling
+    (300, 300, 5, 5, 1e-3, 20, 4_000, 1, 0),   # paper shape D=300, K=5, window=5
+    (120, 128, 8, 15, 1e-3, 1000, 6_000, 1, 1),  # cfg4 tile: N<=16, K+1=16, literal l.10
+    (1, 8, 2, 3, 0.0, 10, 100, 1, 0),          # V=1: every draw is the target -> 100-try fallback
+    (40, 512, 2, 4, 0.0, 4096, 4_100, 1, 0),   # max D, max sentence_len, one ragged chunk
+])
+def test_edge_shapes_deterministic(w2v, V, D, window, K, t, L, n, epochs, allow):
+    ids = inputs.Corpus("iid", V, 1.0, 99).tokens(0, n)
+    g = run_gpu(w2v, ids, V, D, window, K, 0.05, t, 7, L, epochs=epochs, debug=(0, n),
+                opts={"allow_target_negative": allow})
+    o_in, o_out, o_st, o_dbg = oracle.train(ids, V, D, window, K, 0.05, t, 7, L, epochs=epochs,
+                                            allow_target_negative=bool(allow), debug=(0, n))
+    if epochs == 1:
+        assert_stream_equal(g["dbg"], o_dbg)
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert g["stats"][k] == o_st[k], k
+    assert rel_l2(g["M_in"], o_in) <= 1e-5 and rel_l2(g["M_out"], o_out) <= 1e-5
+
+
+def test_host_pointer_and_empty_and_bad_ids(w2v):
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, 3000)
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, device=False)
+    w2v.finalize()
+    o_in, o_out, _, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
+    assert rel_l2(g["M_in"], o_in) <= 1e-5 and rel_l2(g["M_out"], o_out) <= 1e-5
+    # n = 0: success, model unchanged
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    a = np.empty((cfg.V, cfg.D), np.float32); w2v.get_embeddings(0, a)
+    w2v.train(torch.zeros(0, dtype=torch.int32, device="cuda"), 0, 1)
+    b = np.empty_like(a); w2v.get_embeddings(0, b)
+    assert np.array_equal(a, b)
+    # id outside [0,V): EINVAL, nothing trained
+    bad = torch.from_numpy(ids.copy()); bad[1234] = cfg.V
+    with pytest.raises(w2v.W2VError) as e:
+        w2v.train(bad.cuda(), bad.numel(), 1)
+    assert e.value.code == w2v.EINVAL
+    w2v.get_embeddings(0, b)
+    assert np.array_equal(a, b)
+    with pytest.raises(w2v.W2VError):
+        w2v.set_option("no_such_key", 1)
+    # world 1: sync is a no-op
+    w2v.dist_init(0, 1, None)
+    w2v.sync()
+    w2v.get_embeddings(0, b)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ cfg2 Hogwild -------------
+def recall_at_k(M, words, C, k=10):
+    X = M / np.maximum(np.linalg.norm(M, axis=1, keepdims=True), 1e-30)
+    S = X[words] @ X.T
+    S[np.arange(len(words)), words] = -np.inf
+    nn = np.argpartition(-S, k, axis=1)[:, :k]
+    return float(np.mean((nn % C) == (np.asarray(words)[:, None] % C)))
+
+
+def test_cfg2_hogwild_loss_and_recall(w2v):
+    """BASELINE cfg2 shape (V=71,000, D=300, planted C=1,000, window=5, K=5, t=1e-4) on a
+    2^20-token prefix: Hogwild GPU loss within 1% of the sequential oracle's, recall@10 of
+    same-cluster neighbours within 0.02, batch stream bit-exact."""
+    cfg = inputs.CONFIGS[2]
+    n = 1 << 20
+    ids = cfg.corpus().tokens(0, n)
+    dbgw = (n // 2, 4000)
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, mode=0, debug=dbgw)
+    o_in, _, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                        prec="f32", debug=dbgw)
+    assert_stream_equal(g["dbg"], o_dbg)
+    assert g["stats"]["row_touches"] == o_st["row_touches"]
+    gl = g["stats"]["loss_sum"] / g["stats"]["loss_pairs"]
+    ol = o_st["loss_sum"] / o_st["loss_pairs"]
+    print(f"cfg2 prefix loss/pair GPU {gl:.6f} oracle {ol:.6f}")
+    assert abs(gl / ol - 1) < 0.01
+    words = np.arange(300)
+    rg, ro = recall_at_k(g["M_in"].astype(np.float64), words, 1000), recall_at_k(o_in.astype(np.float64), words, 1000)
+    print(f"recall@10 GPU {rg:.4f} oracle {ro:.4f}")
+    assert abs(rg - ro) <= 0.02 and ro > 0.3
+
+
+# ------------------------------------------------------------------ full size, sampled -------
+def test_cfg3_full_size_sampled_stream(w2v):
+    """BASELINE cfg3 at full size (V=1M, D=300, 800M planted tokens) in the bench's launch
+    configuration: the batch stream in three sampled windows is bit-exact with the oracle (which
+    computes thresholds and sampler from its own full-corpus counts); statistics are consistent."""
+    cfg = inputs.CONFIGS[3]
+    ids = cfg.corpus().tokens(0, cfg.n)
+    wins = [(0, 2000), (cfg.n // 2 + 7, 3000), (cfg.n - 2500, 2500)]
+    c = oracle.counts(ids, cfg.V)
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("sentence_len", cfg.L)
+    dev = torch.from_numpy(ids).cuda()
+    outs = []
+    for base, ln in wins:
+        w2v.set_option("debug_base", base)
+        w2v.set_option("debug_len", ln)
+        w2v.train(dev, cfg.n, 1)
+        d = {"keep": np.zeros(ln, np.uint8), "b": np.zeros(ln, np.uint8), "N": np.zeros(ln, np.uint8),
+             "ctx": np.zeros((ln, 2 * cfg.window), np.int32), "neg": np.zeros((ln, cfg.K), np.int32)}
+        w2v.debug_batches(d["keep"], d["b"], d["N"], d["ctx"], d["neg"])
+        outs.append((d, w2v.get_stats()))
+    M = np.empty((cfg.V, cfg.D), np.float32)
+    w2v.get_embeddings(0, M)
+    assert np.isfinite(M).all()
+    for (base, ln), (d, st) in zip(wins, outs):
+        lo = base // cfg.L * cfg.L
+        hi = min(((base + ln + cfg.L - 1) // cfg.L) * cfg.L, cfg.n)
+        o = oracle.batches(ids[lo:hi], cfg.V, cfg.window, cfg.K, cfg.t, cfg.seed, cfg.L, (base, ln),
+                           counts_global=c, ids_base=lo, n_global=cfg.n)
+        assert_stream_equal(d, o)
+    st = outs[-1][1]
+    assert st["words"] == 3 * cfg.n
+    assert 0.5 < st["targets"] / st["words"] < 0.6
+    assert st["loss_sum"] / st["loss_pairs"] < math.log(2)

@@ -1,0 +1,61 @@
+"""CPU-side checks of the C-ABI library (no GPU needed): it loads, exports every symbol that
+include/w2v.h declares, rejects out-of-order calls, and its pure-host C13 planner agrees with
+the oracle's replica protocol."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def binding():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    from paper_1611_06172_b200 import binding as b
+    return b
+
+
+def test_exports_every_declared_symbol(binding):
+    hdr = open(os.path.join(ROOT, "include", "w2v.h")).read()
+    declared = set(re.findall(r"\b(w2v_[a-z_]+)\s*\(", hdr))
+    assert {"w2v_init", "w2v_train", "w2v_sync", "w2v_get_embeddings"} <= declared
+    for name in declared:
+        assert hasattr(binding._lib, name), name
+
+
+def test_out_of_order_calls_rejected(binding):
+    with pytest.raises(binding.W2VError) as e:
+        binding.set_option("mode", 1)
+    assert e.value.code == binding.ESTATE
+    with pytest.raises(binding.W2VError) as e:
+        binding._check(binding._lib.w2v_train(None, 10, 1))
+    assert e.value.code == binding.ESTATE
+    with pytest.raises(binding.W2VError) as e:
+        binding.get_stats()
+    assert e.value.code == binding.ESTATE
+    assert binding.finalize() == 0          # safe when not initialised
+
+
+def test_init_argument_validation(binding):
+    for args in [(0, 32, 2, 3), (10, 30, 2, 3), (10, 32, 0, 3), (10, 32, 2, -1), (10, 32, 2, 32), (10, 1024, 2, 3)]:
+        with pytest.raises(binding.W2VError) as e:
+            binding.init(*args, 0.025, 0.0, 1)
+        assert e.value.code == binding.EINVAL
+    with pytest.raises(binding.W2VError):
+        binding.init(10, 32, 2, 3, 0.0, 0.0, 1)
+    with pytest.raises(binding.W2VError):
+        binding.init(10, 32, 2, 3, 0.025, -1.0, 1)
+
+
+def test_dist_plan_matches_oracle_protocol(binding):
+    from oracle import dist as odist
+    for n, L, W, P in [(23_456, 50, 2, 2_000), (1_000_000, 20, 8, 1 << 16), (999, 1000, 3, 100),
+                       (800_000_000, 20, 8, 1 << 20), (8_000_000_000, 1000, 8, 1 << 18)]:
+        for r in range(W):
+            assert binding.dist_plan(n, L, W, r, P)[:64] == odist.sync_intervals(n, L, W, r, P)[:64]
+            lo, hi = odist.shard_chunks(n, L, W, r)
+            assert binding.dist_shard(n, L, W, r) == (lo * L, min(hi * L, n))
+    with pytest.raises(binding.W2VError):
+        binding.dist_plan(10, 0, 1, 0, 5)
