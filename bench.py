@@ -152,7 +152,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = inputs.CONFIGS[CFG]
-    n = cfg.n
+    n = args.tokens if args.tokens else cfg.n      # --tokens: profiling only (prefix of cfg3)
     start, end = w2v.dist_shard(n, cfg.L, world, rank)
     n_local = end - start
     host = torch.empty(max(n_local, 1), dtype=torch.int32, pin_memory=True)
@@ -227,7 +227,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "cfg3: V=1,000,000 D=300 window=5 K=5 t=1e-4 alpha=0.025, 800M planted "
                                    "Zipf(1.07) tokens (C=10,000, L=20), 1 epoch per step",
-                       "V": cfg.V, "D": cfg.D, "n_tokens": n, "sync_period_words": SYNC_P if world > 1 else None,
+                       "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": SYNC_P if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
                        "mode": "hogwild"},
@@ -261,6 +261,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -70,6 +70,8 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          [base, base+len) during the next w2v_train (len 0 = off)
  *  "l2_persist"            0/1 persisting-L2 access window over the hot-row prefix (a8; default 1)
  *  "ctas_per_sm"           0 = occupancy maximum (default), else that many 1-warp CTAs per SM
+ *  "launch_words"          raw words per hogbatch_step launch (>=1; default 2^26): bounds a
+ *                          launch's duration; results do not depend on it in deterministic mode
  *  "epochs_total"          E used by the alpha schedule when training is split over several
  *                          w2v_train calls (0 = the epochs argument of each call; default 0)
  * Unknown key or bad value -> EINVAL. */

@@ -86,6 +86,7 @@ struct Ctx {
     int l2_persist = 1;
     int ctas_per_sm = 0;
     int32_t epochs_total = 0;
+    int64_t launch_words = 1ll << 26;
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -215,6 +216,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "debug_len") { if (v < 0) return fail(W2V_EINVAL, "debug_len must be >= 0"); g.dbg_len = v; }
     else if (k == "l2_persist") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "l2_persist must be 0/1"); g.l2_persist = (int)v; }
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
+    else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
     else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
     return W2V_OK;
@@ -381,13 +383,20 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         p.epoch = e;
         const int64_t J = g.world > 1 ? pl.J : 1;
         for (int64_t k = 0; k < J; ++k) {
-            p.chunk_lo = g.world > 1 ? chunk_lo + k * pl.I : chunk_lo;
-            p.chunk_hi = (g.world > 1 && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
-            CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
+            const int64_t ilo = g.world > 1 ? chunk_lo + k * pl.I : chunk_lo;
+            const int64_t ihi = (g.world > 1 && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
+            // an interval is issued as launches of at most launch_words raw words (bounded
+            // kernel duration; chunks are still claimed in corpus order inside each launch)
+            const int64_t per = std::max<int64_t>(1, g.launch_words / g.L);
             CU(mark(0));
-            CU(launch_step(p, ctas, st));
-            ++launches;
-            ++g.st.step_launches;
+            for (int64_t a = ilo; a < ihi; a += per) {
+                p.chunk_lo = a;
+                p.chunk_hi = std::min(ihi, a + per);
+                CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
+                CU(launch_step(p, ctas, st));
+                ++launches;
+                ++g.st.step_launches;
+            }
             CU(mark(0));
             if (g.world > 1) {
                 CU(mark(1));
