@@ -26,14 +26,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None) -> str:
+    """Build libw2v.so (or an experiment variant `out` with `extra` nvcc flags)."""
+    target = out or SO
+    if out is None and not force and not _stale():
         return SO
     os.makedirs(BUILD, exist_ok=True)
+    tag = "" if out is None else os.path.basename(out).replace(".so", "") + "_"
 
     def compile_one(src):
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(BUILD, tag + src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -44,16 +47,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         res = list(ex.map(compile_one, SOURCES))
     objs = [o for o, _ in res]
-    tmp = SO + ".tmp"
+    tmp = target + ".tmp"
     r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"],
                        capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, SO)
+    os.replace(tmp, target)
     if verbose:
         for _, err in res:
             print(err)
-    return SO
+    return target
 
 
 if __name__ == "__main__":

@@ -12,7 +12,7 @@ import os
 
 import numpy as np
 
-_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libw2v.so")
+_SO = os.environ.get("W2V_LIBRARY") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libw2v.so")
 if not os.path.exists(_SO):
     raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
 _lib = ctypes.CDLL(_SO)

@@ -176,26 +176,38 @@ def recall_at_k(M, words, C, k=10):
     return float(np.mean((nn % C) == (np.asarray(words)[:, None] % C)))
 
 
+def heldout_loss(M_in, M_out, cfg, n0, n):
+    """SGNS loss per pair of a FROZEN model (alpha = 0) on held-out tokens [n0, n0+n) of the
+    same generator, evaluated by the oracle (identical batches for both models)."""
+    ids = cfg.corpus().tokens(n0, n)
+    _, _, st, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, 0.0, cfg.t, cfg.seed + 1, cfg.L,
+                               model=(M_in, M_out))
+    return st["loss_sum"] / st["loss_pairs"]
+
+
 def test_cfg2_hogwild_loss_and_recall(w2v):
-    """BASELINE cfg2 shape (V=71,000, D=300, planted C=1,000, window=5, K=5, t=1e-4) on a
-    2^20-token prefix: Hogwild GPU loss within 1% of the sequential oracle's, recall@10 of
-    same-cluster neighbours within 0.02, batch stream bit-exact."""
+    """BASELINE cfg2 (V=71,000, D=300, 17M planted tokens, C=1,000, window=5, K=5, t=1e-4), full
+    size, Hogwild GPU (all SMs) vs the sequential oracle: training loss and held-out loss within
+    1%, recall@10 of same-cluster neighbours within 0.02, batch stream bit-exact on a window."""
     cfg = inputs.CONFIGS[2]
-    n = 1 << 20
+    n = cfg.n
     ids = cfg.corpus().tokens(0, n)
     dbgw = (n // 2, 4000)
     g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, mode=0, debug=dbgw)
-    o_in, _, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
-                                        prec="f32", debug=dbgw)
+    o_in, o_out, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed,
+                                            cfg.L, prec="f32", debug=dbgw)
     assert_stream_equal(g["dbg"], o_dbg)
     assert g["stats"]["row_touches"] == o_st["row_touches"]
     gl = g["stats"]["loss_sum"] / g["stats"]["loss_pairs"]
     ol = o_st["loss_sum"] / o_st["loss_pairs"]
-    print(f"cfg2 prefix loss/pair GPU {gl:.6f} oracle {ol:.6f}")
-    assert abs(gl / ol - 1) < 0.01
+    hg = heldout_loss(g["M_in"], g["M_out"], cfg, n, 200_000)
+    ho = heldout_loss(o_in, o_out, cfg, n, 200_000)
     words = np.arange(300)
-    rg, ro = recall_at_k(g["M_in"].astype(np.float64), words, 1000), recall_at_k(o_in.astype(np.float64), words, 1000)
-    print(f"recall@10 GPU {rg:.4f} oracle {ro:.4f}")
+    rg, ro = recall_at_k(g["M_in"].astype(np.float64), words, cfg.C), recall_at_k(o_in.astype(np.float64), words, cfg.C)
+    print(f"cfg2 train loss/pair GPU {gl:.6f} oracle {ol:.6f}; held-out GPU {hg:.6f} oracle {ho:.6f}; "
+          f"recall@10 GPU {rg:.4f} oracle {ro:.4f}")
+    assert abs(gl / ol - 1) < 0.01
+    assert abs(hg / ho - 1) < 0.01
     assert abs(rg - ro) <= 0.02 and ro > 0.3
 
 

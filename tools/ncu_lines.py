@@ -1,0 +1,35 @@
+"""Summarise an ncu report per CUDA source line: instructions executed and warp-stall samples."""
+import csv
+import subprocess
+import sys
+
+
+def main(rep, top=40):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout.splitlines()
+    rows = list(csv.reader(out))
+    hdr = None
+    lines = []
+    for r in rows:
+        if len(r) > 5 and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr) and r[0] not in ("",):
+            d = dict(zip(hdr, r))
+            try:
+                lines.append((int(d["Line No"]), d["Source"][:90], int(d["Warp Stall Sampling (All Samples)"] or 0),
+                              int(d["Instructions Executed"] or 0),
+                              {k: int(v) for k, v in d.items() if k.startswith("stall_") and "Not Issued" not in k
+                               and v.isdigit() and int(v) > 0}))
+            except (ValueError, KeyError):
+                pass
+    tot_s = sum(x[2] for x in lines) or 1
+    tot_i = sum(x[3] for x in lines) or 1
+    print(f"total samples {tot_s}, instructions {tot_i}")
+    for ln, src, s, i, st in sorted(lines, key=lambda x: -x[2])[:top]:
+        reasons = ", ".join(f"{k[6:]}={v * 100 // max(s, 1)}%" for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:3])
+        print(f"{ln:4d} {100 * s / tot_s:5.1f}% smp {100 * i / tot_i:5.1f}% inst | {src.strip()[:70]:70s} | {reasons}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
