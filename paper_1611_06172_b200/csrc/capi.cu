@@ -87,6 +87,7 @@ struct Ctx {
     int ctas_per_sm = 0;
     int32_t epochs_total = 0;
     int64_t launch_words = 1ll << 26;
+    int64_t loss_tail_from = INT64_MAX;
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -216,6 +217,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "debug_len") { if (v < 0) return fail(W2V_EINVAL, "debug_len must be >= 0"); g.dbg_len = v; }
     else if (k == "l2_persist") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "l2_persist must be 0/1"); g.l2_persist = (int)v; }
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
+    else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
     else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
@@ -353,6 +355,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.alpha0 = g.alpha; p.Q = g.Q; p.seed = g.seed; p.V = g.V;
     p.thr = g.thr; p.P = g.P; p.G = g.G; p.info = g.info; p.M = g.M;
     p.chunk_ctr = g.chunk_ctr; p.stats = g.dstats;
+    p.loss_tail_from = g.loss_tail_from;
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
     const size_t wb = step_warp_bytes(g.L, g.window, g.K, g.D, &p.slab_offset);
@@ -432,6 +435,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     g.st.row_touches += (int64_t)hs.row_touches;
     g.st.loss_pairs += (int64_t)hs.loss_pairs;
     g.st.loss_sum += hs.loss_sum;
+    g.st.loss_tail_sum += hs.loss_tail_sum;
+    g.st.loss_tail_pairs += (int64_t)hs.loss_tail_pairs;
     g.st.launches = launches;
     g.st.bytes_row = (int64_t)hs.row_touches * 4 * g.D * 2;
     return W2V_OK;

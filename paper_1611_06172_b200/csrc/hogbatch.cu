@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
     unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0;
     float st_loss_f = 0.f;
-    double st_loss = 0.0;
+    double st_loss = 0.0, st_tail = 0.0;
+    unsigned long long st_tail_pairs = 0;
 
     // C7 negatives + C6 context of kept target m into rowid[0..N+K]
     auto prepare = [&](int m, int nk, int64_t c0, int32_t* rowid) -> Tgt {
@@ -290,6 +291,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             bulk_commit();
             st_loss += (double)st_loss_f;   // per-target partial (<= N terms) into fp64 (C11)
+            if (t.pp >= p.loss_tail_from) {
+                st_tail += (double)st_loss_f;
+                if (lane == 0) st_tail_pairs += (unsigned long long)N * KP1;
+            }
             st_loss_f = 0.f;
             if (lane == 0) {
                 st_targets += 1;
@@ -315,13 +320,20 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
     // flush per-warp statistics
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) st_loss += __shfl_xor_sync(kFull, st_loss, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        st_loss += __shfl_xor_sync(kFull, st_loss, o);
+        st_tail += __shfl_xor_sync(kFull, st_tail, o);
+    }
     if (lane == 0) {
         atomicAdd(&p.stats->words, st_words);
         atomicAdd(&p.stats->targets, st_targets);
         atomicAdd(&p.stats->row_touches, st_touch);
         atomicAdd(&p.stats->loss_pairs, st_pairs);
         atomicAdd(&p.stats->loss_sum, st_loss);
+        if (st_tail_pairs) {
+            atomicAdd(&p.stats->loss_tail_sum, st_tail);
+            atomicAdd(&p.stats->loss_tail_pairs, st_tail_pairs);
+        }
     }
 }
 

@@ -16,6 +16,8 @@ struct SetupInfo {
 struct DevStats {
     unsigned long long words, targets, row_touches, loss_pairs;
     double loss_sum;
+    double loss_tail_sum;
+    unsigned long long loss_tail_pairs;
 };
 
 struct StepParams {
@@ -37,6 +39,7 @@ struct StepParams {
     float* M;  // interleaved model: row w = [M_in[w] (D) | M_out[w] (D)]
     unsigned long long* chunk_ctr;
     DevStats* stats;
+    int64_t loss_tail_from;
     int64_t dbg_base, dbg_len;
     uint8_t *dbg_keep, *dbg_b, *dbg_N;
     int32_t *dbg_ctx, *dbg_neg;
