@@ -46,16 +46,20 @@ struct Pow2 {
     static constexpr int lg = v == 1 ? 0 : v == 2 ? 1 : v == 4 ? 2 : v == 8 ? 3 : v == 16 ? 4 : 5;
 };
 
-// Per-target state produced ahead of time by prepare() (double-buffered rowid lists).
-struct Tgt {
-    int m, N;
-    int64_t pp;
-};
+constexpr int kSampWin = 32;  // ring of sampled targets (negatives staged in smem)
+constexpr int kSampGrp = 8;   // targets sampled together (independent L2 chains in flight)
+
+__device__ __forceinline__ float2 f2fma(float s, float2 a, float2 b) {
+    return make_float2(fmaf(s, a.x, b.x), fmaf(s, a.y, b.y));
+}
 
 #ifndef W2V_MINB
 #define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for
 #endif
-template <int CPL, int KP1MAX>
+
+// CP2 = float2 columns per lane (lane owns d = 2*(lane + 32*c2) + {0,1}, D <= 64*CP2);
+// KP1MAX >= K+1 (register tile of the K+1 output rows).
+template <int CP2, int KP1MAX>
 __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int P2 = Pow2<KP1MAX>::v, LG = Pow2<KP1MAX>::lg, SH = 5 - LG;
@@ -63,9 +67,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase);
     const int D = p.D, K = p.K, KP1 = K + 1, window = p.window, RMAX = 2 * window + KP1;
+    const int KS = K > 0 ? K : 1;
     int32_t* kid = reinterpret_cast<int32_t*>(wbase + 16);   // kept ids of the chunk
     int32_t* kinfo = kid + p.L;                               // (offset << 8) | b
     int32_t* rowid0 = kinfo + p.L;                            // 2 x RMAX: ctx ids, target, negatives
+    int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWin x KS sampled negatives
     float* slab = reinterpret_cast<float*>(wbase + p.slab_offset);
     const uint32_t rowbytes = (uint32_t)D * 4u;
 
@@ -79,50 +85,84 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     __syncwarp();
     uint32_t phase = 0;
 
-    unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0;
+    unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0, st_tail_pairs = 0;
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
-    unsigned long long st_tail_pairs = 0;
 
-    // C7 negatives + C6 context of kept target m into rowid[0..N+K]
-    auto prepare = [&](int m, int nk, int64_t c0, int32_t* rowid) -> Tgt {
-        const int info = kinfo[m];
-        const int b = info & 255;
-        const int64_t pp = c0 + (info >> 8);
-        const int32_t tw = kid[m];
-        const int lo = m - b < 0 ? 0 : m - b;
-        const int hi = m + b > nk - 1 ? nk - 1 : m + b;
-        const int N = hi - lo;
-        for (int i = lane; i < N; i += 32) {
-            const int mm = lo + i + (lo + i >= m ? 1 : 0);
-            rowid[i] = kid[mm];
+    // ---- a2 (C7): negatives of kept targets [m_lo, m_lo+cnt) (cnt <= kSampGrp): lane d
+    // evaluates draw d of every target; the guide-table and prefix loads of all targets are
+    // issued together; a ballot then keeps the first K accepted draws of each target.
+    auto sample_group = [&](int m_lo, int cnt, int64_t c0) {
+        int32_t lo[kSampGrp], hi[kSampGrp], tw[kSampGrp];
+        uint64_t x[kSampGrp];
+#pragma unroll
+        for (int t = 0; t < kSampGrp; ++t) {
+            lo[t] = hi[t] = 0; tw[t] = -1; x[t] = 0;
+            if (t < cnt) {
+                const int info = kinfo[m_lo + t];
+                const int64_t pp = c0 + (info >> 8);
+                tw[t] = kid[m_lo + t];
+                const U4 r = philox(p.seed, kTagNeg, e, (uint64_t)pp, (uint32_t)(lane >> 1));
+                const uint64_t u = (lane & 1) ? (((uint64_t)r.w << 32) | r.z) : (((uint64_t)r.y << 32) | r.x);
+                x[t] = __umul64hi(u, PV);
+                const uint64_t kb = x[t] >> gshift;
+                lo[t] = __ldg(p.G + kb);
+                hi[t] = __ldg(p.G + kb + 1);
+            }
         }
-        if (K > 0) {
-            const U4 r = philox(p.seed, kTagNeg, e, (uint64_t)pp, (uint32_t)(lane >> 1));
-            const uint64_t u = (lane & 1) ? (((uint64_t)r.w << 32) | r.z) : (((uint64_t)r.y << 32) | r.x);
-            const int32_t x = invcdf_guided(p.P, p.G, gshift, __umul64hi(u, PV));
-            const bool acc = (x != tw) || p.allow_tn;
+        for (;;) {  // batched binary search, smallest w in [lo,hi] with P[w+1] > x (C3)
+            bool act = false;
+            int32_t mid[kSampGrp];
+            uint64_t pv[kSampGrp];
+#pragma unroll
+            for (int t = 0; t < kSampGrp; ++t) {
+                mid[t] = lo[t] + ((hi[t] - lo[t]) >> 1);
+                pv[t] = 0;
+                if (lo[t] < hi[t]) { pv[t] = __ldg(p.P + mid[t] + 1); act = true; }
+            }
+            if (!__any_sync(kFull, act)) break;
+#pragma unroll
+            for (int t = 0; t < kSampGrp; ++t)
+                if (lo[t] < hi[t]) { if (pv[t] > x[t]) hi[t] = mid[t]; else lo[t] = mid[t] + 1; }
+        }
+#pragma unroll
+        for (int t = 0; t < kSampGrp; ++t) {
+            if (t >= cnt) break;
+            int32_t* out = negs + ((m_lo + t) % kSampWin) * KS;
+            const bool acc = (lo[t] != tw[t]) || p.allow_tn;
             const unsigned am = __ballot_sync(kFull, acc);
             if (__popc(am) >= K) {
                 const int rank = __popc(am & lanemask_lt());
-                if (acc && rank < K) rowid[N + 1 + rank] = x;
+                if (acc && rank < K) out[rank] = lo[t];
             } else if (lane == 0) {
-                // literal C7 (only reached when fewer than K of the first 32 draws are accepted)
+                // literal C7 (only when fewer than K of the first 32 draws are accepted)
+                const int64_t pp = c0 + (kinfo[m_lo + t] >> 8);
                 uint32_t d = 0;
-                for (int k = 1; k <= K; ++k) {
-                    int32_t y = (int32_t)((tw + 1) % p.V);
+                for (int k = 0; k < K; ++k) {
+                    int32_t y = (int32_t)((tw[t] + 1) % p.V);
                     for (int tries = 0; tries < 100; ++tries, ++d) {
                         const U4 rr = philox(p.seed, kTagNeg, e, (uint64_t)pp, d >> 1);
                         const uint64_t uu = (d & 1) ? (((uint64_t)rr.w << 32) | rr.z) : (((uint64_t)rr.y << 32) | rr.x);
                         const int32_t z = invcdf_guided(p.P, p.G, gshift, __umul64hi(uu, PV));
-                        if (z != tw || p.allow_tn) { y = z; ++d; break; }
+                        if (z != tw[t] || p.allow_tn) { y = z; ++d; break; }
                     }
-                    rowid[N + k] = y;
+                    out[k] = y;
                 }
             }
         }
-        if (lane == 0) rowid[N] = tw;
-        return Tgt{m, N, pp};
+    };
+
+    // ---- C6: context ids, target and its (already sampled) negatives of kept target m
+    auto gather_list = [&](int m, int nk, int32_t* rowid) -> int {
+        const int b = kinfo[m] & 255;
+        const int lo = m - b < 0 ? 0 : m - b;
+        const int hi = m + b > nk - 1 ? nk - 1 : m + b;
+        const int N = hi - lo;
+        for (int i = lane; i < N; i += 32) rowid[i] = kid[lo + i + (lo + i >= m ? 1 : 0)];
+        if (lane == 0) rowid[N] = kid[m];
+        const int32_t* ng = negs + (m % kSampWin) * KS;
+        for (int k = lane; k < K; k += 32) rowid[N + 1 + k] = ng[k];
+        return N;
     };
 
     for (;;) {
@@ -159,12 +199,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             if (p.dbg_len && k < cnt && pp >= p.dbg_base && pp < p.dbg_base + p.dbg_len) {
                 const int64_t q = pp - p.dbg_base;
-                const int kk = K > 0 ? K : 1;
                 p.dbg_keep[q] = keep;
                 p.dbg_b[q] = keep ? (uint8_t)b : 0;
                 p.dbg_N[q] = 0;
                 for (int u = 0; u < 2 * window; ++u) p.dbg_ctx[q * 2 * window + u] = -1;
-                for (int u = 0; u < kk; ++u) p.dbg_neg[q * kk + u] = -1;
+                for (int u = 0; u < KS; ++u) p.dbg_neg[q * KS + u] = -1;
             }
             nk += __popc(m);
         }
@@ -172,25 +211,20 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         __syncwarp();
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
-        // alpha (C8) for the chunk's first quantum and the next one (a chunk spans <= 2 quanta
-        // only when L > Q; the general case is handled by recomputing below)
-        const int64_t pi0 = (int64_t)p.epoch * p.n_local + (c0 - p.shard_start);
-        int64_t qcur = pi0 / p.Q;
-        auto alpha_of = [&](int64_t qidx) -> float {
-            const int64_t num = (int64_t)p.world * qidx * p.Q;
-            const double frac = __ddiv_rn((double)num, (double)alpha_den);
-            return (float)__dmul_rn((double)p.alpha0, fmax(1.0 - frac, 1e-4));
-        };
-        float alpha_cur = alpha_of(qcur);
+        // alpha (C8): recomputed only when a target crosses into the next Q-quantum
+        int64_t q_next = -1;
+        float alpha = 0.f;
 
-        // ---------------- per kept target, in order; negatives of target m+1 are drawn while
-        // the rows of target m are in flight
-        int buf = 0;
-        Tgt t = prepare(0, nk, c0, rowid0);
+        int samp_hi = nk < kSampGrp ? nk : kSampGrp;
+        if (K > 0) sample_group(0, samp_hi, c0);
         __syncwarp();
-        for (;;) {
+        int buf = 0;
+        int N = gather_list(0, nk, rowid0);
+        __syncwarp();
+        for (int m = 0; m < nk; ++m) {
             int32_t* rowid = rowid0 + buf * RMAX;
-            const int N = t.N, R = N + KP1;
+            const int R = N + KP1;
+            const int64_t pp = c0 + (kinfo[m] >> 8);
             // ---------------- a3: gather the snapshot rows (one bulk copy per row)
             if (lane == 0) mbar_arrive_expect_tx(mbar, (uint32_t)R * rowbytes);
             __syncwarp();
@@ -198,47 +232,56 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 const int32_t id = rowid[r];
                 bulk_g2s(slab + r * D, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar);
             }
-            const bool has_next = t.m + 1 < nk;
-            Tgt tn{};
-            if (has_next) tn = prepare(t.m + 1, nk, c0, rowid0 + (buf ^ 1) * RMAX);
-            const int64_t pi = (int64_t)p.epoch * p.n_local + (t.pp - p.shard_start);
-            if (pi / p.Q != qcur) { qcur = pi / p.Q; alpha_cur = alpha_of(qcur); }
-            const float alpha = alpha_cur;
+            // while the rows fly: sample ahead, build the next target's row list, alpha
+            if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kSampGrp) {
+                const int c = nk - samp_hi < kSampGrp ? nk - samp_hi : kSampGrp;
+                sample_group(samp_hi, c, c0);
+                samp_hi += c;
+            }
+            __syncwarp();
+            const int Nn = (m + 1 < nk) ? gather_list(m + 1, nk, rowid0 + (buf ^ 1) * RMAX) : 0;
+            const int64_t pi = (int64_t)p.epoch * p.n_local + (pp - p.shard_start);
+            if (pi >= q_next) {
+                const int64_t qi = pi / p.Q;
+                q_next = (qi + 1) * p.Q;
+                const double frac = __ddiv_rn((double)((int64_t)p.world * qi * p.Q), (double)alpha_den);
+                alpha = (float)__dmul_rn((double)p.alpha0, fmax(1.0 - frac, 1e-4));
+            }
             mbar_wait(mbar, phase);
             phase ^= 1u;
 
             // ---------------- a4-a6: C = A·Bᵀ, E, G, ΔIn (over A), ΔOut (registers, then over B)
-            float bq[KP1MAX][CPL], dq[KP1MAX][CPL];
+            float2 bq[KP1MAX][CP2], dq[KP1MAX][CP2];
             float* Bs = slab + N * D;
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const int d = lane + 32 * c;
-                    bq[j][c] = (j < KP1 && d < D) ? Bs[j * D + d] : 0.f;
-                    dq[j][c] = 0.f;
+                for (int c = 0; c < CP2; ++c) {
+                    const int d = 2 * (lane + 32 * c);
+                    bq[j][c] = (j < KP1 && d < D) ? *reinterpret_cast<const float2*>(Bs + j * D + d) : make_float2(0.f, 0.f);
+                    dq[j][c] = make_float2(0.f, 0.f);
                 }
-            const int jj = (lane >> SH) & (P2 - 1);   // the dot this lane holds after the reduce-scatter
+            const int jj = (lane >> SH) & (P2 - 1);  // the dot this lane holds after the reduce-scatter
             for (int i = 0; i < N; ++i) {
                 float* Ai = slab + i * D;
-                float a[CPL];
+                float2 a[CP2];
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const int d = lane + 32 * c;
-                    a[c] = d < D ? Ai[d] : 0.f;
+                for (int c = 0; c < CP2; ++c) {
+                    const int d = 2 * (lane + 32 * c);
+                    a[c] = d < D ? *reinterpret_cast<const float2*>(Ai + d) : make_float2(0.f, 0.f);
                 }
                 float v[P2];
 #pragma unroll
                 for (int j = 0; j < P2; ++j) {
-                    float s2 = 0.f;
+                    float s0 = 0.f, s1 = 0.f;
                     if (j < KP1MAX) {
 #pragma unroll
-                        for (int c = 0; c < CPL; ++c) s2 = fmaf(a[c], bq[j][c], s2);
+                        for (int c = 0; c < CP2; ++c) { s0 = fmaf(a[c].x, bq[j][c].x, s0); s1 = fmaf(a[c].y, bq[j][c].y, s1); }
                     }
-                    v[j] = s2;
+                    v[j] = s0 + s1;
                 }
-                // butterfly reduce-scatter: after LG halving steps lane holds dot jj (partial over
-                // the lanes sharing jj), then plain xor-sums finish it
+                // butterfly reduce-scatter: LG halving steps leave lane with dot jj (partial),
+                // plain xor-sums over the 2^SH lanes sharing jj finish it
 #pragma unroll
                 for (int st = 0; st < LG; ++st) {
                     const int o = 16 >> st;
@@ -254,32 +297,36 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 float dot = v[0];
 #pragma unroll
                 for (int o = (1 << SH) >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(kFull, dot, o);
-                // E = label - sigma(C) (exact sigma, one per lane), G = alpha * E
-                const float sg = 1.0f / (1.0f + expf(-dot));
-                const float gl = (jj < KP1) ? alpha * ((jj == 0 ? 1.0f : 0.0f) - sg) : 0.f;
-                if (jj < KP1 && (lane & ((1 << SH) - 1)) == 0) st_loss_f += softplus_f(jj == 0 ? -dot : dot);
+                // E = label - sigma(C), G = alpha E; loss softplus(-+C) = max(-+C,0) - log(1/(1+e^-|C|))
+                const float ex = expf(-fabsf(dot));
+                const float rc = __frcp_rn(1.0f + ex);
+                const float sg = dot >= 0.f ? rc : ex * rc;
+                const bool pos = (jj == 0);
+                const float gl = (jj < KP1) ? alpha * ((pos ? 1.0f : 0.0f) - sg) : 0.f;
+                if (jj < KP1 && (lane & ((1 << SH) - 1)) == 0)
+                    st_loss_f += fmaxf(pos ? -dot : dot, 0.f) - __logf(rc);
                 float g[KP1MAX];
 #pragma unroll
                 for (int j = 0; j < KP1MAX; ++j) g[j] = __shfl_sync(kFull, gl, j << SH);
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const int d = lane + 32 * c;
-                    float s2 = 0.f;
+                for (int c = 0; c < CP2; ++c) {
+                    const int d = 2 * (lane + 32 * c);
+                    float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int j = 0; j < KP1MAX; ++j) s2 = fmaf(g[j], bq[j][c], s2);
-                    if (d < D) Ai[d] = s2;
+                    for (int j = 0; j < KP1MAX; ++j) s2 = f2fma(g[j], bq[j][c], s2);
+                    if (d < D) *reinterpret_cast<float2*>(Ai + d) = s2;
                 }
 #pragma unroll
                 for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
-                    for (int c = 0; c < CPL; ++c) dq[j][c] = fmaf(g[j], a[c], dq[j][c]);
+                    for (int c = 0; c < CP2; ++c) dq[j][c] = f2fma(g[j], a[c], dq[j][c]);
             }
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const int d = lane + 32 * c;
-                    if (j < KP1 && d < D) Bs[j * D + d] = dq[j][c];
+                for (int c = 0; c < CP2; ++c) {
+                    const int d = 2 * (lane + 32 * c);
+                    if (j < KP1 && d < D) *reinterpret_cast<float2*>(Bs + j * D + d) = dq[j][c];
                 }
             fence_proxy_async_smem();
             __syncwarp();
@@ -291,7 +338,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             bulk_commit();
             st_loss += (double)st_loss_f;   // per-target partial (<= N terms) into fp64 (C11)
-            if (t.pp >= p.loss_tail_from) {
+            if (pp >= p.loss_tail_from) {
                 st_tail += (double)st_loss_f;
                 if (lane == 0) st_tail_pairs += (unsigned long long)N * KP1;
             }
@@ -301,8 +348,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 st_touch += (unsigned long long)R;
                 st_pairs += (unsigned long long)N * KP1;
             }
-            if (p.dbg_len && t.pp >= p.dbg_base && t.pp < p.dbg_base + p.dbg_len) {
-                const int64_t q = t.pp - p.dbg_base;
+            if (p.dbg_len && pp >= p.dbg_base && pp < p.dbg_base + p.dbg_len) {
+                const int64_t q = pp - p.dbg_base;
                 if (lane == 0) p.dbg_N[q] = (uint8_t)N;
                 for (int i = lane; i < N; i += 32) p.dbg_ctx[q * 2 * window + i] = rowid[i];
                 for (int k = lane; k < K; k += 32) p.dbg_neg[q * K + k] = rowid[N + 1 + k];
@@ -312,8 +359,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             bulk_wait_all();
             if (p.deterministic) __threadfence();
             __syncwarp();
-            if (!has_next) break;
-            t = tn;
+            N = Nn;
             buf ^= 1;
         }
     }
@@ -340,28 +386,28 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 using KernelFn = void (*)(const StepParams);
 
 struct Inst {
-    int cpl, kp1;
+    int cp2, kp1;
     KernelFn fn;
 };
 
 #define W2V_INST(C, KK) {C, KK, hogbatch_step_kernel<C, KK>}
-// (columns-per-lane, max K+1) instantiations; register footprint ~ 2*CPL*KP1MAX floats.
+// (float2 columns per lane, max K+1) instantiations; register tile ~ 4*CP2*KP1MAX floats.
 const Inst kInst[] = {
-    W2V_INST(1, 2),  W2V_INST(1, 4),  W2V_INST(1, 6),  W2V_INST(1, 8),  W2V_INST(1, 16), W2V_INST(1, 32),
-    W2V_INST(2, 2),  W2V_INST(2, 4),  W2V_INST(2, 6),  W2V_INST(2, 8),  W2V_INST(2, 16), W2V_INST(2, 32),
-    W2V_INST(4, 2),  W2V_INST(4, 4),  W2V_INST(4, 6),  W2V_INST(4, 8),  W2V_INST(4, 16),
-    W2V_INST(8, 2),  W2V_INST(8, 4),  W2V_INST(8, 6),  W2V_INST(8, 8),
-    W2V_INST(10, 2), W2V_INST(10, 4), W2V_INST(10, 6), W2V_INST(10, 8),
-    W2V_INST(16, 2), W2V_INST(16, 4), W2V_INST(16, 6),
+    W2V_INST(1, 2), W2V_INST(1, 4), W2V_INST(1, 6), W2V_INST(1, 8), W2V_INST(1, 16), W2V_INST(1, 32),
+    W2V_INST(2, 2), W2V_INST(2, 4), W2V_INST(2, 6), W2V_INST(2, 8), W2V_INST(2, 16),
+    W2V_INST(3, 2), W2V_INST(3, 4), W2V_INST(3, 6), W2V_INST(3, 8),
+    W2V_INST(4, 2), W2V_INST(4, 4), W2V_INST(4, 6), W2V_INST(4, 8),
+    W2V_INST(5, 2), W2V_INST(5, 4), W2V_INST(5, 6), W2V_INST(5, 8),
+    W2V_INST(8, 2), W2V_INST(8, 4),
 };
 #undef W2V_INST
 
 const Inst* pick(int D, int K) {
-    const int cpl_need = (D + 31) / 32, kp1 = K + 1;
+    const int need = (D + 63) / 64, kp1 = K + 1;
     const Inst* best = nullptr;
     for (const Inst& in : kInst) {
-        if (in.cpl < cpl_need || in.kp1 < kp1) continue;
-        if (!best || in.cpl * in.kp1 < best->cpl * best->kp1) best = &in;
+        if (in.cp2 < need || in.kp1 < kp1) continue;
+        if (!best || in.cp2 * in.kp1 < best->cp2 * best->kp1) best = &in;
     }
     return best;
 }
@@ -371,11 +417,12 @@ const Inst* pick(int D, int K) {
 bool step_supported(int D, int K) { return pick(D, K) != nullptr; }
 
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
-    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)] [slab (2w+K+1) x D fp32]
-    const size_t ids = 16 + (size_t)(2 * L + 2 * (2 * window + K + 1)) * 4;
+    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)][negs 32 x max(K,1)] [slab (2w+K+1) x D fp32]
+    const int R = 2 * window + K + 1;
+    const size_t ids = 16 + (size_t)(2 * L + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4;
     const size_t off = (ids + 127) / 128 * 128;
     if (slab_offset) *slab_offset = (int32_t)off;
-    return off + (size_t)(2 * window + K + 1) * D * 4;
+    return off + (size_t)R * D * 4;
 }
 
 int step_max_ctas_per_sm(const StepParams& p) {
