@@ -56,7 +56,9 @@ typedef struct {
  * maximum half-window of C4; N <= 2*window), K shared negatives (0..31; K=0 degenerates to
  * logistic regression), alpha initial learning rate (>0, C8), subsample t (>=0,
  * C2; 0 disables), seed (C1 key). Initialises M_in ~ U[-0.5/D, 0.5/D) and M_out = 0 per C9.
- * Errors: EINVAL on out-of-range arguments or unsupported (D, K),
+ * Supported (D, K) envelope of the register tiles: D <= 64 with K <= 31, D <= 192 with
+ * K <= 15, D <= 320 with K <= 7, D <= 512 with K <= 5 (covers the paper's D=300, K=5).
+ * Errors: EINVAL on out-of-range arguments or (D, K) outside the envelope,
  * ENOMEM naming the 2*V*D*4 bytes requested, ESTATE if already initialised. */
 int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float subsample,
              uint64_t seed);

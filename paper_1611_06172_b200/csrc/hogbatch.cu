@@ -12,9 +12,11 @@
 //   a3  gather the N context rows of M_in and the K+1 rows of M_out into the warp's smem slab:
 //       one bulk copy (cp.async.bulk, the TMA engine) per row, completing on an mbarrier —
 //       the snapshot of R11, no register staging, ~1 instruction per row
-//   a4  C = A·Bᵀ: lane owns columns d = lane + 32c; B and the ΔOut accumulators live in
-//       registers; the N x (K+1) partial dots are finished by a butterfly reduce-scatter
-//       (lane ends with one dot), fp32 FMA — no tensor cores: tiles are <= 16x16
+//   a4  C = A·Bᵀ: lane owns float2 columns d = 2·lane + 64c; B and the ΔOut accumulators live
+//       in registers; rows are zero-padded to 64·CP2 floats in smem so no predicates remain;
+//       packed fp32 FMA (FFMA2, fma.rn.f32x2 — two IEEE fmaf per issue slot); the N x (K+1)
+//       partial dots are finished by a butterfly reduce-scatter (lane ends with one dot). No
+//       tensor cores: the tiles are <= 16x16 (fp32 parity would also need 3xTF32)
 //   a5  E = [j=0] − σ(C) once per lane, G = αE broadcast by shuffles; loss in fp64
 //   a6  ΔIn_i = G_i·B written over A_i in smem; ΔOut_j += G_ij·A_i in registers, then over B_j
 //   a7  Hogwild scatter: one bulk fp32 reduce-add per row
@@ -49,8 +51,14 @@ struct Pow2 {
 constexpr int kSampWin = 32;  // ring of sampled targets (negatives staged in smem)
 constexpr int kSampGrp = 8;   // targets sampled together (independent L2 chains in flight)
 
-__device__ __forceinline__ float2 f2fma(float s, float2 a, float2 b) {
-    return make_float2(fmaf(s, a.x, b.x), fmaf(s, a.y, b.y));
+// Blackwell packed fp32 FMA (FFMA2): two IEEE fmaf's, one issue slot.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
 }
 
 #ifndef W2V_MINB
@@ -72,7 +80,9 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     int32_t* kinfo = kid + p.L;                               // (offset << 8) | b
     int32_t* rowid0 = kinfo + p.L;                            // 2 x RMAX: ctx ids, target, negatives
     int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWin x KS sampled negatives
-    float* slab = reinterpret_cast<float*>(wbase + p.slab_offset);
+    constexpr int RS = 64 * CP2;                             // padded smem row stride (floats)
+    float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
+    float* As = Bs + KP1MAX * RS;                             // 2*window rows: context
     const uint32_t rowbytes = (uint32_t)D * 4u;
 
     const uint64_t PV = p.info->PV;
@@ -82,6 +92,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     const int64_t alpha_den = (int64_t)p.epochs * p.n_global + 1;
 
     if (lane == 0) mbar_init(mbar, 1);
+    for (int i = lane; i < (KP1MAX + 2 * window) * RS / 4; i += 32)
+        reinterpret_cast<float4*>(Bs)[i] = make_float4(0.f, 0.f, 0.f, 0.f);  // padding stays 0
     __syncwarp();
     uint32_t phase = 0;
 
@@ -230,7 +242,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             __syncwarp();
             for (int r = lane; r < R; r += 32) {
                 const int32_t id = rowid[r];
-                bulk_g2s(slab + r * D, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar);
+                float* dst = r < N ? As + r * RS : Bs + (r - N) * RS;
+                bulk_g2s(dst, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar);
             }
             // while the rows fly: sample ahead, build the next target's row list, alpha
             if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kSampGrp) {
@@ -251,34 +264,31 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             phase ^= 1u;
 
             // ---------------- a4-a6: C = A·Bᵀ, E, G, ΔIn (over A), ΔOut (registers, then over B)
+            // Rows are padded to RS floats and B to KP1MAX rows with zeros (never written by
+            // the bulk copies), so the compute needs no column or row predicates.
             float2 bq[KP1MAX][CP2], dq[KP1MAX][CP2];
-            float* Bs = slab + N * D;
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) {
-                    const int d = 2 * (lane + 32 * c);
-                    bq[j][c] = (j < KP1 && d < D) ? *reinterpret_cast<const float2*>(Bs + j * D + d) : make_float2(0.f, 0.f);
+                    bq[j][c] = *reinterpret_cast<const float2*>(Bs + j * RS + 2 * lane + 64 * c);
                     dq[j][c] = make_float2(0.f, 0.f);
                 }
             const int jj = (lane >> SH) & (P2 - 1);  // the dot this lane holds after the reduce-scatter
             for (int i = 0; i < N; ++i) {
-                float* Ai = slab + i * D;
+                float* Ai = As + i * RS + 2 * lane;
                 float2 a[CP2];
 #pragma unroll
-                for (int c = 0; c < CP2; ++c) {
-                    const int d = 2 * (lane + 32 * c);
-                    a[c] = d < D ? *reinterpret_cast<const float2*>(Ai + d) : make_float2(0.f, 0.f);
-                }
+                for (int c = 0; c < CP2; ++c) a[c] = *reinterpret_cast<const float2*>(Ai + 64 * c);
                 float v[P2];
 #pragma unroll
                 for (int j = 0; j < P2; ++j) {
-                    float s0 = 0.f, s1 = 0.f;
+                    float2 s2 = make_float2(0.f, 0.f);
                     if (j < KP1MAX) {
 #pragma unroll
-                        for (int c = 0; c < CP2; ++c) { s0 = fmaf(a[c].x, bq[j][c].x, s0); s1 = fmaf(a[c].y, bq[j][c].y, s1); }
+                        for (int c = 0; c < CP2; ++c) s2 = ffma2(a[c], bq[j][c], s2);
                     }
-                    v[j] = s0 + s1;
+                    v[j] = s2.x + s2.y;
                 }
                 // butterfly reduce-scatter: LG halving steps leave lane with dot jj (partial),
                 // plain xor-sums over the 2^SH lanes sharing jj finish it
@@ -305,36 +315,37 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 const float gl = (jj < KP1) ? alpha * ((pos ? 1.0f : 0.0f) - sg) : 0.f;
                 if (jj < KP1 && (lane & ((1 << SH) - 1)) == 0)
                     st_loss_f += fmaxf(pos ? -dot : dot, 0.f) - __logf(rc);
-                float g[KP1MAX];
+                float2 g2[KP1MAX];
 #pragma unroll
-                for (int j = 0; j < KP1MAX; ++j) g[j] = __shfl_sync(kFull, gl, j << SH);
+                for (int j = 0; j < KP1MAX; ++j) {
+                    const float gj = __shfl_sync(kFull, gl, j << SH);
+                    g2[j] = make_float2(gj, gj);
+                }
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) {
-                    const int d = 2 * (lane + 32 * c);
                     float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int j = 0; j < KP1MAX; ++j) s2 = f2fma(g[j], bq[j][c], s2);
-                    if (d < D) *reinterpret_cast<float2*>(Ai + d) = s2;
+                    for (int j = 0; j < KP1MAX; ++j) s2 = ffma2(g2[j], bq[j][c], s2);
+                    *reinterpret_cast<float2*>(Ai + 64 * c) = s2;
                 }
 #pragma unroll
                 for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
-                    for (int c = 0; c < CP2; ++c) dq[j][c] = f2fma(g[j], a[c], dq[j][c]);
+                    for (int c = 0; c < CP2; ++c) dq[j][c] = ffma2(g2[j], a[c], dq[j][c]);
             }
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
-                for (int c = 0; c < CP2; ++c) {
-                    const int d = 2 * (lane + 32 * c);
-                    if (j < KP1 && d < D) *reinterpret_cast<float2*>(Bs + j * D + d) = dq[j][c];
-                }
+                for (int c = 0; c < CP2; ++c)
+                    *reinterpret_cast<float2*>(Bs + j * RS + 2 * lane + 64 * c) = dq[j][c];
             fence_proxy_async_smem();
             __syncwarp();
 
             // ---------------- a7: Hogwild scatter-add, one bulk fp32 reduction per row at L2
             for (int r = lane; r < R; r += 32) {
                 const int32_t id = rowid[r];
-                bulk_red_add_s2g(p.M + (size_t)id * 2 * D + (r < N ? 0 : D), slab + r * D, rowbytes);
+                const float* src = r < N ? As + r * RS : Bs + (r - N) * RS;
+                bulk_red_add_s2g(p.M + (size_t)id * 2 * D + (r < N ? 0 : D), src, rowbytes);
             }
             bulk_commit();
             st_loss += (double)st_loss_f;   // per-target partial (<= N terms) into fp64 (C11)
@@ -395,11 +406,14 @@ struct Inst {
 const Inst kInst[] = {
     W2V_INST(1, 2), W2V_INST(1, 4), W2V_INST(1, 6), W2V_INST(1, 8), W2V_INST(1, 16), W2V_INST(1, 32),
     W2V_INST(2, 2), W2V_INST(2, 4), W2V_INST(2, 6), W2V_INST(2, 8), W2V_INST(2, 16),
-    W2V_INST(3, 2), W2V_INST(3, 4), W2V_INST(3, 6), W2V_INST(3, 8),
+    W2V_INST(3, 2), W2V_INST(3, 4), W2V_INST(3, 6), W2V_INST(3, 8), W2V_INST(3, 16),
     W2V_INST(4, 2), W2V_INST(4, 4), W2V_INST(4, 6), W2V_INST(4, 8),
     W2V_INST(5, 2), W2V_INST(5, 4), W2V_INST(5, 6), W2V_INST(5, 8),
-    W2V_INST(8, 2), W2V_INST(8, 4),
+    W2V_INST(8, 2), W2V_INST(8, 4), W2V_INST(8, 6),
 };
+// Supported envelope (w2v_init rejects the rest): ceil(D/64) float2 columns per lane times
+// the padded K+1 tile must be one of the rows above, i.e. D <= 64 with K <= 31; D <= 128 with
+// K <= 15; D <= 192 with K <= 15; D <= 320 with K <= 7; D <= 512 with K <= 5.
 #undef W2V_INST
 
 const Inst* pick(int D, int K) {
@@ -417,12 +431,15 @@ const Inst* pick(int D, int K) {
 bool step_supported(int D, int K) { return pick(D, K) != nullptr; }
 
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
-    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)][negs 32 x max(K,1)] [slab (2w+K+1) x D fp32]
+    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)][negs 32 x max(K,1)]
+    // [slab: KP1MAX B rows + 2w A rows, stride 64*CP2 fp32]
+    const Inst* in = pick(D, K);
+    if (!in) return 0;
     const int R = 2 * window + K + 1;
     const size_t ids = 16 + (size_t)(2 * L + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4;
     const size_t off = (ids + 127) / 128 * 128;
     if (slab_offset) *slab_offset = (int32_t)off;
-    return off + (size_t)R * D * 4;
+    return off + (size_t)(in->kp1 + 2 * window) * 64 * in->cp2 * 4;
 }
 
 int step_max_ctas_per_sm(const StepParams& p) {
