@@ -163,6 +163,7 @@ def run_ours(args):
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", SYNC_P)
+    w2v.set_option("kernel", args.kernel)
     stream = torch.cuda.current_stream()
     w2v.set_stream(stream.cuda_stream)
     if world > 1:
@@ -230,7 +231,7 @@ def run_ours(args):
                        "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": SYNC_P if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
-                       "mode": "hogwild"},
+                       "mode": "hogwild", "kernel": {1: "rows", 2: "window"}.get(last["kernel"])},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "hogbatch_step",
                          "peak_source": peak_src,
@@ -261,6 +262,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 per-target rows, 2 window-resident rows")
     ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
     args = ap.parse_args()
     if args.impl == "reference":

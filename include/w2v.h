@@ -49,6 +49,7 @@ typedef struct {
     int64_t bytes_row;    /* algorithmic row bytes of the last w2v_train: row_touches*4D*2      */
     double  loss_tail_sum;   /* loss of targets at global positions >= option loss_tail_from    */
     int64_t loss_tail_pairs; /* ... and their pair count (the "final-10%" training loss)         */
+    int64_t kernel;          /* fused-step kernel of the last w2v_train: 1 rows, 2 window        */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").
@@ -76,6 +77,9 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "ctas_per_sm"           0 = occupancy maximum (default), else that many 1-warp CTAs per SM
  *  "launch_words"          raw words per hogbatch_step launch (>=1; default 2^26): bounds a
  *                          launch's duration; results do not depend on it in deterministic mode
+ *  "kernel"                0 auto (default: window-resident rows when window <= 15 and the
+ *                          window fits in shared memory, else per-target rows), 1 per-target
+ *                          rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
  *  "loss_tail_from"        global position from which targets also accumulate into
  *                          loss_tail_sum / loss_tail_pairs (default: never)
  *  "epochs_total"          E used by the alpha schedule when training is split over several

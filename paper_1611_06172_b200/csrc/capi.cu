@@ -88,6 +88,7 @@ struct Ctx {
     int32_t epochs_total = 0;
     int64_t launch_words = 1ll << 26;
     int64_t loss_tail_from = INT64_MAX;
+    int kernel = 0;  // 0 auto, 1 per-target rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -218,6 +219,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "l2_persist") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "l2_persist must be 0/1"); g.l2_persist = (int)v; }
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
+    else if (k == "kernel") { if (v < 0 || v > 2) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows) or 2 (window)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
     else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
@@ -358,16 +360,27 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.loss_tail_from = g.loss_tail_from;
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
-    const size_t wb = step_warp_bytes(g.L, g.window, g.K, g.D, &p.slab_offset);
-    if (wb > 227 * 1024) return fail(W2V_EINVAL, "w2v_train: per-warp shared memory %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
+    // kernel choice: window-resident rows when the window fits, else per-target
+    int32_t off_win = 0, off_row = 0;
+    const size_t wb_win = win_warp_bytes(g.L, g.window, g.K, g.D, &off_win);
+    const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row);
+    const size_t kSmemMax = 227 * 1024;
+    bool use_win = wb_win > 0 && wb_win <= kSmemMax;
+    if (g.kernel == 1) use_win = false;
+    if (g.kernel == 2 && !use_win)
+        return fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
+    const size_t wb = use_win ? wb_win : wb_row;
+    p.slab_offset = use_win ? off_win : off_row;
+    if (wb == 0 || wb > kSmemMax) return fail(W2V_EINVAL, "w2v_train: per-warp shared memory %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
     p.warp_bytes = (int32_t)wb;
     int ctas = 1;
     if (g.mode == 0) {
-        int occ = step_max_ctas_per_sm(p);
+        int occ = use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
         if (occ < 1) return fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per warp)", wb);
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
+    g.st.kernel = use_win ? 2 : 1;
     CU(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
@@ -396,7 +409,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 p.chunk_lo = a;
                 p.chunk_hi = std::min(ihi, a + per);
                 CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
-                CU(launch_step(p, ctas, st));
+                CU(use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));
                 ++launches;
                 ++g.st.step_launches;
             }

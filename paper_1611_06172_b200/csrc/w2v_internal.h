@@ -55,7 +55,12 @@ cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T
                           int* launches);
 cudaError_t launch_init(float* M, int64_t V, int32_t D, uint64_t seed, int sms, cudaStream_t st);
 
-// hogbatch.cu
+// hogbatch_win.cu (window-resident rows; window <= 15)
+size_t win_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
+int win_max_ctas_per_sm(const StepParams& p);
+cudaError_t launch_win(const StepParams& p, int ctas, cudaStream_t st);
+
+// hogbatch.cu (per-target rows; any window)
 bool step_supported(int D, int K);
 cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st);
 int step_max_ctas_per_sm(const StepParams& p);

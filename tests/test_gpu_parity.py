@@ -79,13 +79,19 @@ def test_init_bitexact(w2v):
 
 
 # ------------------------------------------------------------------ cfg1 parity --------------
+KERNELS = [1, 2]   # 1 = per-target rows (hogbatch.cu), 2 = window-resident rows (hogbatch_win.cu)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("n", [1000, 5000, 20000])
-def test_cfg1_deterministic_parity(w2v, n):
+def test_cfg1_deterministic_parity(w2v, n, kernel):
     """BASELINE cfg1 (V=1000, D=32, window=2, K=3, t=0, Zipf(1.0)): bit-exact batch stream and
     <=1e-5 relative L2 of both matrices against the fp64 oracle after n raw tokens."""
     cfg = inputs.CONFIGS[1]
     ids = cfg.corpus().tokens(0, n)
-    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, n))
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, n),
+                opts={"kernel": kernel})
+    assert g["stats"]["kernel"] == kernel
     o_in, o_out, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
                                             debug=(0, n))
     assert_stream_equal(g["dbg"], o_dbg)
@@ -100,7 +106,8 @@ def test_cfg1_deterministic_parity(w2v, n):
     assert e_in <= 1e-5 and e_out <= 1e-5
 
 
-def test_cfg1_hogwild_stream_and_loss(w2v):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_cfg1_hogwild_stream_and_loss(w2v, kernel):
     """Hogwild mode (persistent grid, all SMs) on cfg1: the batch stream does not depend on the
     model, so it stays bit-exact. cfg1 has only 20 chunks, all trained concurrently from the
     initial model (Hogwild "can reduce the rate of convergence"), so the loss bar
@@ -108,7 +115,7 @@ def test_cfg1_hogwild_stream_and_loss(w2v):
     cfg = inputs.CONFIGS[1]
     ids = cfg.corpus().tokens(0, cfg.n)
     g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, mode=0,
-                debug=(0, cfg.n))
+                debug=(0, cfg.n), opts={"kernel": kernel})
     _, _, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
                                      debug=(0, cfg.n))
     assert_stream_equal(g["dbg"], o_dbg)
@@ -124,11 +131,14 @@ def test_cfg1_hogwild_stream_and_loss(w2v):
     (120, 128, 8, 15, 1e-3, 1000, 6_000, 1, 1),  # cfg4 tile: N<=16, K+1=16, literal l.10
     (1, 8, 2, 3, 0.0, 10, 100, 1, 0),          # V=1: every draw is the target -> 100-try fallback
     (40, 512, 2, 4, 0.0, 4096, 4_100, 1, 0),   # max D, max sentence_len, one ragged chunk
+    (30, 8, 15, 1, 0.0, 300, 2_000, 1, 0),     # largest window of the window-resident kernel
 ])
-def test_edge_shapes_deterministic(w2v, V, D, window, K, t, L, n, epochs, allow):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_edge_shapes_deterministic(w2v, V, D, window, K, t, L, n, epochs, allow, kernel):
     ids = inputs.Corpus("iid", V, 1.0, 99).tokens(0, n)
     g = run_gpu(w2v, ids, V, D, window, K, 0.05, t, 7, L, epochs=epochs, debug=(0, n),
-                opts={"allow_target_negative": allow})
+                opts={"allow_target_negative": allow, "kernel": kernel})
+    assert g["stats"]["kernel"] == kernel
     o_in, o_out, o_st, o_dbg = oracle.train(ids, V, D, window, K, 0.05, t, 7, L, epochs=epochs,
                                             allow_target_negative=bool(allow), debug=(0, n))
     if epochs == 1:
@@ -204,7 +214,8 @@ def oracle_train_tail(ids, cfg, tail_from, prec="f32", debug=None):
     return M_in, M_out, tot, tail.as_dict(), dbg
 
 
-def test_cfg2_hogwild_loss_and_recall(w2v):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_cfg2_hogwild_loss_and_recall(w2v, kernel):
     """BASELINE cfg2 (V=71,000, D=300, 17M planted tokens, C=1,000, window=5, K=5, t=1e-4), full
     size, Hogwild GPU (all SMs) vs the sequential oracle: final-10% training
     loss and held-out loss within 1%, recall@10 of same-cluster neighbours within 0.02, batch
@@ -216,7 +227,7 @@ def test_cfg2_hogwild_loss_and_recall(w2v):
     dbgw = (n // 2, 4000)
     tail_from = (n * 9 // 10) // cfg.L * cfg.L
     g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, mode=0, debug=dbgw,
-                opts={"loss_tail_from": tail_from})
+                opts={"loss_tail_from": tail_from, "kernel": kernel})
     o_in, o_out, o_st, o_tail, o_dbg = oracle_train_tail(ids, cfg, tail_from, debug=dbgw)
     assert_stream_equal(g["dbg"], o_dbg)
     assert g["stats"]["row_touches"] == o_st["row_touches"]
