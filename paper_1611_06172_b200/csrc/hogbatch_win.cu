@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
     uint32_t freem = 0, newslots = 0, bytesA = 0;
+    int32_t pend_exit = -1;  // M_in row whose write-back is in the most recent bulk group
 
     // ---- window bookkeeping (uniform: every lane executes it with identical values)
     auto enter = [&](int q) {  // plan the entry of kept position q; the copy is issued later
@@ -118,7 +119,10 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
             slot_ref[s] = ref;
             if (ref == 0) bulk_red_add_s2g(p.M + (size_t)slot_id[s] * 2 * D, acc + s * RS, rowbytes);
         }
-        if (ref == 0) freem |= 1u << s;
+        if (ref == 0) {
+            freem |= 1u << s;
+            pend_exit = slot_id[s];
+        }
         __syncwarp();
     };
     auto issue_B = [&](int m, int buf) {  // target + negatives of kept target m into Bb[buf]
@@ -149,11 +153,12 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         __syncwarp();
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
-        // every gather below must see all of this warp's earlier reductions
-        bulk_wait_all();
-        __syncwarp();
         int samp_hi = nk < kSampGrp ? nk : kSampGrp;
         if (K > 0) sample_group(p, 0, samp_hi, c0, kid, kinfo, negs, PV, gshift, lane);
+        // every gather below must see all of this warp's earlier reductions
+        bulk_wait_all();
+        pend_exit = -1;
+        __syncwarp();
         for (int i = lane; i < S; i += 32) slot_ref[i] = 0;
         freem = (S >= 32) ? 0xffffffffu : ((1u << S) - 1u);
         __syncwarp();
@@ -189,14 +194,29 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
                 }
             }
             // ---------------- prefetch for target m+1 (overlaps this target's compute)
-            bulk_wait_all();  // reductions of target m-1 done: Bp reusable, freed slots reusable
-            __syncwarp();
             if (K > 0 && samp_hi < nk && samp_hi - (m + 2) < kSampGrp) {
                 const int c = nk - samp_hi < kSampGrp ? nk - samp_hi : kSampGrp;
                 sample_group(p, samp_hi, c, c0, kid, kinfo, negs, PV, gshift, lane);
                 samp_hi += c;
                 __syncwarp();
             }
+            // Sources of earlier reductions must be read before Bp / freed slots are reused, and
+            // every group but target m-1's must be complete; a gather that touches a row still in
+            // target m-1's group (same M_out id, or the M_in row it wrote back) waits for it.
+            bulk_wait_read_all();
+            bulk_wait_all_but_last();
+            if (m + 1 < nk) {
+                bool conf = false;
+                if (lane < KP1) {
+                    const int32_t id = lane == 0 ? kid[m + 1] : negs[((m + 1) % kSampWin) * KS + lane - 1];
+                    const int32_t* bidp = bid + nxt * KP1MAX;
+                    for (int jp = 0; jp < KP1; ++jp) conf |= (id == bidp[jp]);
+                }
+                if (lane == 0 && m + w + 1 < nk) conf |= (kid[m + w + 1] == pend_exit);
+                if (__any_sync(kFull, conf)) bulk_wait_all();
+            }
+            pend_exit = -1;
+            __syncwarp();
             if (m + 1 < nk) {  // one arrival per wait on each barrier
                 issue_B(m + 1, nxt);
                 if (m + w + 1 < nk) enter(m + w + 1);
