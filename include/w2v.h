@@ -77,9 +77,9 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "ctas_per_sm"           0 = occupancy maximum (default), else that many 1-warp CTAs per SM
  *  "launch_words"          raw words per hogbatch_step launch (>=1; default 2^26): bounds a
  *                          launch's duration; results do not depend on it in deterministic mode
- *  "kernel"                0 auto (default: window-resident rows when window <= 15 and the
- *                          window fits in shared memory, else per-target rows), 1 per-target
- *                          rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
+ *  "kernel"                0 auto (default; currently = 1, the faster on B200 for the paper's
+ *                          shapes), 1 per-target rows (hogbatch.cu), 2 window-
+ *                          resident rows (hogbatch_win.cu; window <= 15)
  *  "loss_tail_from"        global position from which targets also accumulate into
  *                          loss_tail_sum / loss_tail_pairs (default: never)
  *  "epochs_total"          E used by the alpha schedule when training is split over several

@@ -366,7 +366,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row);
     const size_t kSmemMax = 227 * 1024;
     bool use_win = wb_win > 0 && wb_win <= kSmemMax;
-    if (g.kernel == 1) use_win = false;
+    if (g.kernel != 2) use_win = false;  // auto = per-target rows (measured faster)
     if (g.kernel == 2 && !use_win)
         return fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
     const size_t wb = use_win ? wb_win : wb_row;
