@@ -34,7 +34,7 @@ namespace w2v {
 namespace {
 
 #ifndef W2V_MINB
-#define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for
+#define W2V_MINB 10  // resident 1-warp CTAs per SM the register budget is sized for (smem allows 10)
 #endif
 
 // CP2 = float2 columns per lane (lane owns d = 2*(lane + 32*c2) + {0,1}, D <= 64*CP2);
@@ -42,7 +42,7 @@ namespace {
 template <int CP2, int KP1MAX>
 __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int P2 = Pow2<KP1MAX>::v, LG = Pow2<KP1MAX>::lg, SH = 5 - LG;
+    constexpr int TI = 32 / KP1MAX;  // inputs per reduce-scatter tile
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase);
@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     int32_t* kinfo = kid + p.L;                               // (offset << 8) | b
     int32_t* rowid0 = kinfo + p.L;                            // 2 x RMAX: ctx ids, target, negatives
     int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWin x KS sampled negatives
+    float* gs = reinterpret_cast<float*>(negs + kSampWin * KS);  // G of the target, [N][KP1MAX]
     constexpr int RS = 64 * CP2;                             // padded smem row stride (floats)
     float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
     float* As = Bs + KP1MAX * RS;                             // 2*window rows: context
@@ -142,7 +143,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
             // ---------------- a4-a6: C = A·Bᵀ, E, G, ΔIn (over A), ΔOut (registers, then over B)
             // Rows are padded to RS floats and B to KP1MAX rows with zeros (never written by
-            // the bulk copies), so the compute needs no column or row predicates.
+            // the bulk copies), so the compute needs no column or row predicates. Inputs go in
+            // tiles of TI = 32/KP1MAX: the TI*KP1MAX partial dots of a tile are finished by ONE
+            // butterfly reduce-scatter (lane l ends with dot l = t*KP1MAX + j), σ/G/loss once per
+            // lane, G through smem; then per input: ΔOut += G·A (snapshot) and ΔIn over A.
             float2 bq[KP1MAX][CP2], dq[KP1MAX][CP2];
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
@@ -151,53 +155,61 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                     bq[j][c] = *reinterpret_cast<const float2*>(Bs + j * RS + 2 * lane + 64 * c);
                     dq[j][c] = make_float2(0.f, 0.f);
                 }
-            const int jj = (lane >> SH) & (P2 - 1);  // the dot this lane holds after the reduce-scatter
+            const int tt = lane / KP1MAX, tj = lane - tt * KP1MAX;  // dot held after the reduce-scatter
+            for (int i0 = 0; i0 < N; i0 += TI) {
+                float v[32];
+#pragma unroll
+                for (int t = 0; t < TI; ++t) {
+                    const float* Ai = As + (i0 + t < N ? i0 + t : 0) * RS + 2 * lane;
+                    float2 a[CP2];
+#pragma unroll
+                    for (int c = 0; c < CP2; ++c) a[c] = *reinterpret_cast<const float2*>(Ai + 64 * c);
+#pragma unroll
+                    for (int j = 0; j < KP1MAX; ++j) {
+                        float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int c = 0; c < CP2; ++c) s2 = ffma2(a[c], bq[j][c], s2);
+                        v[t * KP1MAX + j] = s2.x + s2.y;
+                    }
+                }
+#pragma unroll
+                for (int u = TI * KP1MAX; u < 32; ++u) v[u] = 0.f;
+#pragma unroll
+                for (int st = 0; st < 5; ++st) {
+                    const int o = 16 >> st;
+                    const bool up = lane & o;
+#pragma unroll
+                    for (int u = 0; u < o; ++u) {
+                        const float send = up ? v[u] : v[u + o];
+                        const float keep = up ? v[u + o] : v[u];
+                        v[u] = keep + __shfl_xor_sync(kFull, send, o);
+                    }
+                }
+                const float dot = v[0];
+                const bool valid = tt < TI && i0 + tt < N && tj < KP1;
+                const float ex = expf(-fabsf(dot));
+                const float rc = __frcp_rn(1.0f + ex);
+                const float sg = dot >= 0.f ? rc : ex * rc;
+                const bool pos = (tj == 0);
+                if (lane < TI * KP1MAX) gs[i0 * KP1MAX + lane] = valid ? alpha * ((pos ? 1.0f : 0.0f) - sg) : 0.f;
+                if (valid) st_loss_f += fmaxf(pos ? -dot : dot, 0.f) - __logf(rc);
+            }
+            __syncwarp();
             for (int i = 0; i < N; ++i) {
                 float* Ai = As + i * RS + 2 * lane;
                 float2 a[CP2];
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) a[c] = *reinterpret_cast<const float2*>(Ai + 64 * c);
-                float v[P2];
-#pragma unroll
-                for (int j = 0; j < P2; ++j) {
-                    float2 s2 = make_float2(0.f, 0.f);
-                    if (j < KP1MAX) {
-#pragma unroll
-                        for (int c = 0; c < CP2; ++c) s2 = ffma2(a[c], bq[j][c], s2);
-                    }
-                    v[j] = s2.x + s2.y;
-                }
-                // butterfly reduce-scatter: LG halving steps leave lane with dot jj (partial),
-                // plain xor-sums over the 2^SH lanes sharing jj finish it
-#pragma unroll
-                for (int st = 0; st < LG; ++st) {
-                    const int o = 16 >> st;
-                    const int half = P2 >> (st + 1);
-                    const bool up = lane & o;
-#pragma unroll
-                    for (int u = 0; u < half; ++u) {
-                        const float send = up ? v[u] : v[u + half];
-                        const float keep = up ? v[u + half] : v[u];
-                        v[u] = keep + __shfl_xor_sync(kFull, send, o);
-                    }
-                }
-                float dot = v[0];
-#pragma unroll
-                for (int o = (1 << SH) >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(kFull, dot, o);
-                // E = label - sigma(C), G = alpha E; loss softplus(-+C) = max(-+C,0) - log(1/(1+e^-|C|))
-                const float ex = expf(-fabsf(dot));
-                const float rc = __frcp_rn(1.0f + ex);
-                const float sg = dot >= 0.f ? rc : ex * rc;
-                const bool pos = (jj == 0);
-                const float gl = (jj < KP1) ? alpha * ((pos ? 1.0f : 0.0f) - sg) : 0.f;
-                if (jj < KP1 && (lane & ((1 << SH) - 1)) == 0)
-                    st_loss_f += fmaxf(pos ? -dot : dot, 0.f) - __logf(rc);
                 float2 g2[KP1MAX];
 #pragma unroll
                 for (int j = 0; j < KP1MAX; ++j) {
-                    const float gj = __shfl_sync(kFull, gl, j << SH);
+                    const float gj = gs[i * KP1MAX + j];
                     g2[j] = make_float2(gj, gj);
                 }
+#pragma unroll
+                for (int j = 0; j < KP1MAX; ++j)
+#pragma unroll
+                    for (int c = 0; c < CP2; ++c) dq[j][c] = ffma2(g2[j], a[c], dq[j][c]);
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) {
                     float2 s2 = make_float2(0.f, 0.f);
@@ -205,10 +217,6 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                     for (int j = 0; j < KP1MAX; ++j) s2 = ffma2(g2[j], bq[j][c], s2);
                     *reinterpret_cast<float2*>(Ai + 64 * c) = s2;
                 }
-#pragma unroll
-                for (int j = 0; j < KP1MAX; ++j)
-#pragma unroll
-                    for (int c = 0; c < CP2; ++c) dq[j][c] = ffma2(g2[j], a[c], dq[j][c]);
             }
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
@@ -308,12 +316,14 @@ const Inst* pick(int D, int K) {
 bool step_supported(int D, int K) { return pick(D, K) != nullptr; }
 
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
-    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)][negs 32 x max(K,1)]
+    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)][negs 32 x max(K,1)][G tiles x 32]
     // [slab: KP1MAX B rows + 2w A rows, stride 64*CP2 fp32]
     const Inst* in = pick(D, K);
     if (!in) return 0;
     const int R = 2 * window + K + 1;
-    const size_t ids = 16 + (size_t)(2 * L + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4;
+    const int TI = 32 / in->kp1;
+    const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
+    const size_t ids = 16 + (size_t)(2 * L + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 127) / 128 * 128;
     if (slab_offset) *slab_offset = (int32_t)off;
     return off + (size_t)(in->kp1 + 2 * window) * 64 * in->cp2 * 4;
