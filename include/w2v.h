@@ -124,8 +124,10 @@ int w2v_get_stats(w2v_stats_t* out);
 int w2v_debug_batches(uint8_t* keep, uint8_t* b, uint8_t* N, int32_t* ctx, int32_t* neg);
 
 /* Data-parallel bootstrap (C13). Rank 0 creates a 128-byte NCCL unique id; the caller
- * broadcasts it (torch.distributed) and every rank calls w2v_dist_init. world == 1 needs no
- * id (pass NULL) and makes no NCCL call. Requires libnccl.so.2 (dlopen) when world > 1. */
+ * broadcasts it (torch.distributed) and every rank calls w2v_dist_init. world == 1 with a NULL id
+ * creates no communicator and makes no NCCL call; world == 1 WITH an id creates a 1-rank NCCL
+ * communicator so that every collective of the data-parallel path runs on one GPU (test hook;
+ * averaging one replica is the identity). Requires libnccl.so.2 (dlopen) when an id is given. */
 int w2v_dist_unique_id(uint8_t out[128]);
 int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]);
 

@@ -156,8 +156,13 @@ Plan make_plan(int64_t n, int32_t L, int32_t W, int32_t r, int64_t P) {
     return p;
 }
 
+// The data-parallel path runs whenever a communicator exists: world > 1, or a 1-rank NCCL
+// communicator created by w2v_dist_init(0, 1, id) (test hook: exercises every collective on one
+// GPU; averaging over one replica is the identity).
+bool dp() { return g.comm != nullptr; }
+
 int sync_models() {
-    if (g.world <= 1) return W2V_OK;
+    if (!dp()) return W2V_OK;
     NC(g_nccl.allReduce(g.M, g.M, (size_t)g.V * 2 * g.D, ncclFloat32, ncclAvg, g.comm, g.stream));
     g.st.syncs += 1;
     return W2V_OK;
@@ -242,7 +247,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     g.st.bytes_row = 0;
     // the union of the shards may be non-empty while this rank's shard is empty: only a
     // world-1 empty corpus is a pure no-op
-    if (n == 0 && g.world == 1) return W2V_OK;
+    if (n == 0 && !dp()) return W2V_OK;
     if (!ids_in && n > 0) return fail(W2V_EINVAL, "w2v_train: null corpus");
     cudaStream_t st = g.stream;
     int launches = 0;
@@ -266,7 +271,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaEventRecord(ev_h2d, st));
     // ---- a0: shard geometry (C13), counts, thresholds, sampler
     int64_t n_global = n, shard_start = 0;
-    if (g.world > 1) {
+    if (dp()) {
         if (!g.dp_tmp) { int rc = dmalloc((void**)&g.dp_tmp, (size_t)g.world * 8, "dp scratch"); if (rc) return rc; }
         std::vector<int64_t> h(g.world, 0);
         h[g.rank] = n;
@@ -286,12 +291,12 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaMemsetAsync(g.counts, 0, (size_t)g.V * 8, st));
     CU(cudaMemsetAsync(g.info, 0, sizeof(SetupInfo), st));
     CU(launch_hist(ids, n, g.V, g.counts, g.info, g.sms, st, &launches));
-    if (g.world > 1) NC(g_nccl.allReduce(g.counts, g.counts, (size_t)g.V, ncclUint64, ncclSum, g.comm, st));
+    if (dp()) NC(g_nccl.allReduce(g.counts, g.counts, (size_t)g.V, ncclUint64, ncclSum, g.comm, st));
     CU(launch_tables(g.counts, g.V, n_global, g.t, g.thr, g.P, g.scratch, g.G, g.gbits, g.info, st, &launches));
     SetupInfo hinfo{};
     CU(cudaMemcpyAsync(&hinfo, g.info, sizeof hinfo, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    if (g.world > 1) {
+    if (dp()) {
         // every rank must take the same exit: combine the bad-id flags
         std::vector<int64_t> h(g.world, 0);
         h[g.rank] = hinfo.bad_id;
@@ -397,10 +402,10 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     };
     for (int32_t e = 0; e < epochs; ++e) {
         p.epoch = e;
-        const int64_t J = g.world > 1 ? pl.J : 1;
+        const int64_t J = dp() ? pl.J : 1;
         for (int64_t k = 0; k < J; ++k) {
-            const int64_t ilo = g.world > 1 ? chunk_lo + k * pl.I : chunk_lo;
-            const int64_t ihi = (g.world > 1 && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
+            const int64_t ilo = dp() ? chunk_lo + k * pl.I : chunk_lo;
+            const int64_t ihi = (dp() && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
             // an interval is issued as launches of at most launch_words raw words (bounded
             // kernel duration; chunks are still claimed in corpus order inside each launch)
             const int64_t per = std::max<int64_t>(1, g.launch_words / g.L);
@@ -414,7 +419,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 ++g.st.step_launches;
             }
             CU(mark(0));
-            if (g.world > 1) {
+            if (dp()) {
                 CU(mark(1));
                 int rc = sync_models();
                 if (rc) return rc;
@@ -516,7 +521,7 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
     if (g.comm) return fail(W2V_ESTATE, "w2v_dist_init: already initialised");
     g.rank = rank;
     g.world = world;
-    if (world == 1) return W2V_OK;
+    if (world == 1 && !id) return W2V_OK;  // no communicator, no collective calls
     if (!id) return fail(W2V_EINVAL, "w2v_dist_init: null id with world > 1");
     if (!g_nccl.load()) return fail(W2V_ENCCL, "cannot dlopen libnccl.so.2: %s", dlerror());
     ncclUniqueId uid;
