@@ -50,6 +50,8 @@ typedef struct {
     double  loss_tail_sum;   /* loss of targets at global positions >= option loss_tail_from    */
     int64_t loss_tail_pairs; /* ... and their pair count (the "final-10%" training loss)         */
     int64_t kernel;          /* fused-step kernel of the last w2v_train: 1 rows, 2 window        */
+    double  ms_batch;        /* ... of which the a1/a2 batch kernel (subsampling, windows,
+                                negatives; batch.cu), ms — not included in ms_step              */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").

@@ -26,7 +26,8 @@ class Stats(ctypes.Structure):
                 ("launches", ctypes.c_int64), ("ms_total", ctypes.c_double), ("ms_step", ctypes.c_double),
                 ("ms_setup", ctypes.c_double), ("ms_sync", ctypes.c_double), ("ms_h2d", ctypes.c_double),
                 ("step_launches", ctypes.c_int64), ("bytes_row", ctypes.c_int64),
-                ("loss_tail_sum", ctypes.c_double), ("loss_tail_pairs", ctypes.c_int64), ("kernel", ctypes.c_int64)]
+                ("loss_tail_sum", ctypes.c_double), ("loss_tail_pairs", ctypes.c_int64), ("kernel", ctypes.c_int64),
+                ("ms_batch", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

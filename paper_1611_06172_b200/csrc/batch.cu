@@ -1,0 +1,143 @@
+// batch.cu — SURVEY.md §8(a) rows a1 (frequency subsampling + window batching) and a2 (the
+// counter-based-RNG unigram^0.75 negative sampler) as their own kernel, run once per launch
+// range of chunks just before the fused step kernel consumes its output.
+//
+// Why a separate kernel: both rows are chains of dependent L2 loads (thr[ids[p]]; guide table
+// then a binary search over the u64 prefix P). Inside the fused step, whose occupancy is capped
+// by its row slabs (~10 warps/SM), those chains sat on every warp's critical path (r01 ablation:
+// removing the sampler from the step kernel raised cfg3 throughput by 41%). Here they run at
+// full occupancy, where the latency is hidden by other warps, and the step kernel reads a
+// compact batch stream (~30 B per kept target, <0.3% of the row traffic).
+//
+// Output, per chunk s of the launch range (rel = s - chunk_lo; Lp = L rounded up to 4):
+//   bt_nk[rel]                       number of kept positions of the chunk (C2, C5)
+//   bt_kid[rel*Lp + m]               word of kept position m, in corpus order (C6)
+//   bt_kinfo[rel*Lp + m]             (offset of m inside the chunk) << 8 | b   (C4)
+//   bt_neg[(rel*Lp + m)*KS + k]      k-th shared negative of kept target m (C7), written only
+//                                    when the chunk keeps >= 2 positions (else N = 0 for all)
+// plus the keep / b debug records (w2v_debug_batches) for positions in the debug range.
+#include "w2v_device.cuh"
+#include "w2v_internal.h"
+
+namespace w2v {
+
+namespace {
+
+constexpr unsigned kAll = 0xffffffffu;
+constexpr int kBatchWarps = 8;            // warps per CTA
+constexpr int kMaskWords = 4096 / 32;     // sentence_len <= 4096
+
+__device__ __forceinline__ unsigned lane_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// draw d of the NEG stream at position pp (C1: block idx = d >> 1, half d & 1) through C3
+__device__ __forceinline__ int32_t neg_draw(const StepParams& p, uint32_t e, int64_t pp, uint32_t d, uint64_t PV,
+                                            int gshift) {
+    const U4 r = philox(p.seed, kTagNeg, e, (uint64_t)pp, d >> 1);
+    const uint64_t u = (d & 1) ? (((uint64_t)r.w << 32) | r.z) : (((uint64_t)r.y << 32) | r.x);
+    return invcdf_guided(p.P, p.G, gshift, __umul64hi(u, PV));
+}
+
+__global__ void __launch_bounds__(32 * kBatchWarps) batch_kernel(const StepParams p) {
+    __shared__ uint32_t redo[kBatchWarps][kMaskWords];  // targets whose first K draws hit a rejection
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* fix = redo[wid];
+    const uint32_t e = (uint32_t)p.epoch;
+    const int window = p.window, K = p.K, KS = K > 0 ? K : 1, Lp = p.Lp;
+    const int64_t shard_end = p.shard_start + p.n_local;
+    const uint64_t PV = p.info->PV;
+    const int gshift = p.info->gshift;
+    const int64_t nwarps = (int64_t)gridDim.x * kBatchWarps;
+
+    for (int64_t s = p.chunk_lo + (int64_t)blockIdx.x * kBatchWarps + wid; s < p.chunk_hi; s += nwarps) {
+        const int64_t rel = s - p.chunk_lo;
+        int64_t c0 = s * (int64_t)p.L, c1 = c0 + p.L;
+        if (c1 > shard_end) c1 = shard_end;
+        if (c0 < p.shard_start) c0 = p.shard_start;
+        const int cnt = c1 > c0 ? (int)(c1 - c0) : 0;
+        int32_t* kid = p.bt_kid + rel * Lp;
+        int32_t* kinfo = p.bt_kinfo + rel * Lp;
+
+        // ---- a1: keep iff u32(POS,e,p)[0] < thr[ids[p]] (C2); compaction in order; b (C4)
+        int nk = 0;
+        for (int k0 = 0; k0 < cnt; k0 += 32) {
+            const int k = k0 + lane;
+            const int64_t pp = c0 + k;
+            bool keep = false;
+            int32_t w = 0;
+            uint32_t u1 = 0;
+            if (k < cnt) {
+                w = __ldg(p.ids + (pp - p.ids_base));
+                const U4 r = philox(p.seed, kTagPos, e, (uint64_t)pp, 0u);
+                keep = (uint64_t)r.x < __ldg(p.thr + w);
+                u1 = r.y;
+            }
+            const unsigned m = __ballot_sync(kAll, keep);
+            const int b = 1 + (int)(((uint64_t)u1 * (uint64_t)window) >> 32);
+            if (keep) {
+                const int slot = nk + __popc(m & lane_lt());
+                kid[slot] = w;
+                kinfo[slot] = (k << 8) | b;
+            }
+            if (p.dbg_len && k < cnt && pp >= p.dbg_base && pp < p.dbg_base + p.dbg_len) {
+                const int64_t q = pp - p.dbg_base;
+                p.dbg_keep[q] = keep;
+                p.dbg_b[q] = keep ? (uint8_t)b : 0;
+                p.dbg_N[q] = 0;  // the step kernel fills N / ctx / negatives of trained targets
+                for (int u = 0; u < 2 * window; ++u) p.dbg_ctx[q * 2 * window + u] = -1;
+                for (int u = 0; u < KS; ++u) p.dbg_neg[q * KS + u] = -1;
+            }
+            nk += __popc(m);
+        }
+        if (lane == 0) p.bt_nk[rel] = nk;
+        if (nk < 2 || K == 0) continue;  // N = 0 for every kept target iff nk < 2
+        __syncwarp();                    // kid / kinfo written by other lanes are visible below
+
+        // ---- a2: K negatives per kept target (C7). Lane u handles draw d = u % K of target
+        // m = u / K, assuming no rejection before it; a target whose first K draws contain a
+        // rejection (x == target) is redone by one lane with the literal sequential rule.
+        for (int i = lane; i < (nk + 31) / 32; i += 32) fix[i] = 0u;
+        __syncwarp();
+        int32_t* neg = p.bt_neg + rel * Lp * KS;
+        for (int u = lane; u < nk * K; u += 32) {
+            const int m = u / K, d = u - m * K;
+            const int64_t pp = c0 + (kinfo[m] >> 8);
+            const int32_t tw = kid[m];
+            const int32_t x = neg_draw(p, e, pp, (uint32_t)d, PV, gshift);
+            if (x != tw || p.allow_tn) neg[m * KS + d] = x;
+            else atomicOr(fix + (m >> 5), 1u << (m & 31));
+        }
+        __syncwarp();
+        for (int m = lane; m < nk; m += 32) {
+            if (!((fix[m >> 5] >> (m & 31)) & 1u)) continue;
+            const int64_t pp = c0 + (kinfo[m] >> 8);
+            const int32_t tw = kid[m];
+            uint32_t d = 0;
+            for (int k = 0; k < K; ++k) {
+                int32_t y = (int32_t)((tw + 1) % p.V);
+                for (int tries = 0; tries < 100; ++tries) {
+                    const int32_t z = neg_draw(p, e, pp, d++, PV, gshift);
+                    if (z != tw || p.allow_tn) { y = z; break; }
+                }
+                neg[m * KS + k] = y;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_batch(const StepParams& p, int sms, cudaStream_t st) {
+    const int64_t chunks = p.chunk_hi - p.chunk_lo;
+    if (chunks <= 0) return cudaSuccess;
+    int64_t blocks = (chunks + kBatchWarps - 1) / kBatchWarps;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+    batch_kernel<<<(int)blocks, 32 * kBatchWarps, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace w2v

@@ -102,6 +102,9 @@ struct Ctx {
     DevStats* dstats = nullptr;
     unsigned long long* chunk_ctr = nullptr;
     int64_t* dp_tmp = nullptr;
+    // batch stream of one launch range (batch.cu -> step kernels), capacity in chunks
+    int32_t *bt_nk = nullptr, *bt_kid = nullptr, *bt_kinfo = nullptr, *bt_neg = nullptr;
+    size_t bt_cap_nk = 0, bt_cap_kid = 0, bt_cap_neg = 0;
     // debug
     uint8_t *dbg_keep = nullptr, *dbg_b = nullptr, *dbg_N = nullptr;
     int32_t *dbg_ctx = nullptr, *dbg_neg = nullptr;
@@ -112,6 +115,12 @@ struct Ctx {
     // stats
     w2v_stats_t st{};
 } g;
+
+void free_bt() {
+    cudaFree(g.bt_nk); cudaFree(g.bt_kid); cudaFree(g.bt_kinfo); cudaFree(g.bt_neg);
+    g.bt_nk = g.bt_kid = g.bt_kinfo = g.bt_neg = nullptr;
+    g.bt_cap_nk = g.bt_cap_kid = g.bt_cap_neg = 0;
+}
 
 void free_dbg() {
     cudaFree(g.dbg_keep); cudaFree(g.dbg_b); cudaFree(g.dbg_N); cudaFree(g.dbg_ctx); cudaFree(g.dbg_neg);
@@ -125,6 +134,30 @@ int dmalloc(void** p, size_t bytes, const char* what) {
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(W2V_ENOMEM, "cudaMalloc of %zu bytes for %s failed: %s", bytes, what, cudaGetErrorString(e));
+    }
+    return W2V_OK;
+}
+
+// batch stream buffers for `chunks` chunks of Lp slots (batch.cu layout); the negatives are
+// padded by kSampGrp (8) targets because the step kernels prefetch a fixed group past nk
+int ensure_bt(int64_t chunks, int32_t Lp, int32_t KS) {
+    const size_t nk = (size_t)chunks, kid = (size_t)chunks * Lp, neg = (size_t)chunks * Lp * KS + 8 * (size_t)KS;
+    int rc;
+    if (nk > g.bt_cap_nk) {
+        cudaFree(g.bt_nk); g.bt_nk = nullptr; g.bt_cap_nk = 0;
+        if ((rc = dmalloc((void**)&g.bt_nk, nk * 4, "batch stream (kept counts)"))) return rc;
+        g.bt_cap_nk = nk;
+    }
+    if (kid > g.bt_cap_kid) {
+        cudaFree(g.bt_kid); cudaFree(g.bt_kinfo); g.bt_kid = g.bt_kinfo = nullptr; g.bt_cap_kid = 0;
+        if ((rc = dmalloc((void**)&g.bt_kid, kid * 4, "batch stream (kept words)"))) return rc;
+        if ((rc = dmalloc((void**)&g.bt_kinfo, kid * 4, "batch stream (offsets, b)"))) return rc;
+        g.bt_cap_kid = kid;
+    }
+    if (neg > g.bt_cap_neg) {
+        cudaFree(g.bt_neg); g.bt_neg = nullptr; g.bt_cap_neg = 0;
+        if ((rc = dmalloc((void**)&g.bt_neg, neg * 4, "batch stream (negatives)"))) return rc;
+        g.bt_cap_neg = neg;
     }
     return W2V_OK;
 }
@@ -242,7 +275,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     if (epochs < 1) return fail(W2V_EINVAL, "w2v_train: epochs=%d must be >= 1", epochs);
     if (n < 0) return fail(W2V_EINVAL, "w2v_train: n_tokens < 0");
     g.st.launches = 0;
-    g.st.ms_total = g.st.ms_step = g.st.ms_setup = g.st.ms_sync = g.st.ms_h2d = 0;
+    g.st.ms_total = g.st.ms_step = g.st.ms_setup = g.st.ms_sync = g.st.ms_h2d = g.st.ms_batch = 0;
     g.st.step_launches = 0;
     g.st.bytes_row = 0;
     // the union of the shards may be non-empty while this rank's shard is empty: only a
@@ -390,8 +423,17 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
     const int64_t chunk_hi = (shard_start + n + g.L - 1) / g.L;
+    // an interval is issued as launches of at most launch_words raw words (bounded kernel
+    // duration and batch-stream size); chunks are still claimed in corpus order in each launch
+    const int64_t per = std::max<int64_t>(1, g.launch_words / g.L);
+    p.Lp = (g.L + 3) & ~3;
+    {
+        int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, g.K > 0 ? g.K : 1);
+        if (rc) return rc;
+    }
+    p.bt_nk = g.bt_nk; p.bt_kid = g.bt_kid; p.bt_kinfo = g.bt_kinfo; p.bt_neg = g.bt_neg;
     std::vector<cudaEvent_t> evs;
-    std::vector<int> ev_kind;  // 0 step, 1 sync
+    std::vector<int> ev_kind;  // 0 step, 1 sync, 2 batch
     auto mark = [&](int kind) -> cudaError_t {
         cudaEvent_t e;
         cudaError_t r = cudaEventCreate(&e);
@@ -406,19 +448,19 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         for (int64_t k = 0; k < J; ++k) {
             const int64_t ilo = dp() ? chunk_lo + k * pl.I : chunk_lo;
             const int64_t ihi = (dp() && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
-            // an interval is issued as launches of at most launch_words raw words (bounded
-            // kernel duration; chunks are still claimed in corpus order inside each launch)
-            const int64_t per = std::max<int64_t>(1, g.launch_words / g.L);
-            CU(mark(0));
             for (int64_t a = ilo; a < ihi; a += per) {
                 p.chunk_lo = a;
                 p.chunk_hi = std::min(ihi, a + per);
+                CU(mark(2));
+                CU(launch_batch(p, g.sms, st));  // a1 + a2 -> batch stream
+                CU(mark(2));
                 CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
-                CU(use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));
-                ++launches;
+                CU(mark(0));
+                CU(use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a7
+                CU(mark(0));
+                launches += 2;
                 ++g.st.step_launches;
             }
-            CU(mark(0));
             if (dp()) {
                 CU(mark(1));
                 int rc = sync_models();
@@ -444,7 +486,9 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaEventElapsedTime(&ms, ev_h2d, ev_setup)); g.st.ms_setup = ms;
     for (size_t i = 0; i + 1 < evs.size(); i += 2) {
         CU(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
-        if (ev_kind[i] == 0) g.st.ms_step += ms; else g.st.ms_sync += ms;
+        if (ev_kind[i] == 0) g.st.ms_step += ms;
+        else if (ev_kind[i] == 1) g.st.ms_sync += ms;
+        else g.st.ms_batch += ms;
     }
     for (auto e : evs) cudaEventDestroy(e);
     cudaEventDestroy(ev0); cudaEventDestroy(ev_h2d); cudaEventDestroy(ev_setup); cudaEventDestroy(ev_end);
@@ -550,6 +594,7 @@ int w2v_finalize(void) {
     cudaStreamSynchronize(g.stream);
     if (g.comm) g_nccl.commDestroy(g.comm);
     free_dbg();
+    free_bt();
     cudaFree(g.M); cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
     cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
     cudaStreamDestroy(g.own_stream);

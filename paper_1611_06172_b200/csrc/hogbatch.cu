@@ -1,14 +1,9 @@
-// hogbatch.cu — the fused HogBatch step (SURVEY.md §8(a) rows a1-a7), sm_100a.
+// hogbatch.cu — the fused HogBatch step (SURVEY.md §8(a) rows a3-a7), sm_100a.
 //
 // One WARP is one work unit. It claims whole chunks (C5) from a global counter in increasing
-// corpus order and, per chunk:
-//   a1  keep flags (C2) + in-order compaction (ballot/popc) + half-window b (C4), in smem
-//   per kept target, in chunk order (targets of a chunk are sequential, R11):
-//   a2  K shared negatives (C7): lane d evaluates draw d in parallel, a ballot picks the
-//       first K accepted draws (exactly C7's sequential redraw rule when >= K of the first
-//       32 draws are accepted; otherwise a literal sequential fallback). Drawn for target m+1
-//       while the rows of target m are in flight (the sampler's dependent L2 loads overlap
-//       the gather).
+// corpus order. The chunk's batch stream (kept words, offsets/b, shared negatives: rows a1/a2,
+// batch.cu) arrives by cp.async; then per kept target, in chunk order (targets of a chunk are
+// sequential, R11):
 //   a3  gather the N context rows of M_in and the K+1 rows of M_out into the warp's smem slab:
 //       one bulk copy (cp.async.bulk, the TMA engine) per row, completing on an mbarrier —
 //       the snapshot of R11, no register staging, ~1 instruction per row
@@ -17,11 +12,12 @@
 //       packed fp32 FMA (FFMA2, fma.rn.f32x2 — two IEEE fmaf per issue slot); the N x (K+1)
 //       partial dots are finished by a butterfly reduce-scatter (lane ends with one dot). No
 //       tensor cores: the tiles are <= 16x16 (fp32 parity would also need 3xTF32)
-//   a5  E = [j=0] − σ(C) once per lane, G = αE broadcast by shuffles; loss in fp64
+//   a5  E = [j=0] − σ(C) once per lane, G = αE through smem; loss in fp64
 //   a6  ΔIn_i = G_i·B written over A_i in smem; ΔOut_j += G_ij·A_i in registers, then over B_j
 //   a7  Hogwild scatter: one bulk fp32 reduce-add per row
 //       (cp.reduce.async.bulk .add.f32, element-atomic at L2); the warp waits for completion
 //       before the next target's gather so a chunk's targets see each other's updates.
+// The next target's row list and negatives are prepared while the rows fly.
 // Paper mapping: Alg.1 loops over inputs and outputs one dot at a time;
 // HogBatch batches them into C = A·Bᵀ and the two update GEMMs; the
 // "write back at the end of the GEMM" is the scatter of a7.
@@ -46,11 +42,12 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase);
+    int32_t* nk_s = reinterpret_cast<int32_t*>(wbase + 8);   // kept count of the chunk
     const int D = p.D, K = p.K, KP1 = K + 1, window = p.window, RMAX = 2 * window + KP1;
     const int KS = K > 0 ? K : 1;
     int32_t* kid = reinterpret_cast<int32_t*>(wbase + 16);   // kept ids of the chunk
-    int32_t* kinfo = kid + p.L;                               // (offset << 8) | b
-    int32_t* rowid0 = kinfo + p.L;                            // 2 x RMAX: ctx ids, target, negatives
+    int32_t* kinfo = kid + p.Lp;                              // (offset << 8) | b
+    int32_t* rowid0 = kinfo + p.Lp;                           // 2 x RMAX: ctx ids, target, negatives
     int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWin x KS sampled negatives
     float* gs = reinterpret_cast<float*>(negs + kSampWin * KS);  // G of the target, [N][KP1MAX]
     constexpr int RS = 64 * CP2;                             // padded smem row stride (floats)
@@ -58,8 +55,6 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     float* As = Bs + KP1MAX * RS;                             // 2*window rows: context
     const uint32_t rowbytes = (uint32_t)D * 4u;
 
-    const uint64_t PV = p.info->PV;
-    const int gshift = p.info->gshift;
     const int64_t shard_end = p.shard_start + p.n_local;
 
     if (lane == 0) mbar_init(mbar, 1);
@@ -96,19 +91,20 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         const int cnt = (int)(c1 - c0);
         if (cnt <= 0) continue;
 
-        // ---------------- a1: subsampling (C2) + in-order compaction + window (C4)
-        const int nk = compact_chunk(p, c0, cnt, kid, kinfo, lane);
-        if (lane == 0) st_words += (unsigned long long)cnt;
+        // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
+        const int64_t rel = s - p.chunk_lo;
+        load_chunk(p, rel, kid, kinfo, nk_s, negs, lane);
+        cp_async_wait_all();
         __syncwarp();
+        const int nk = *nk_s;
+        if (lane == 0) st_words += (unsigned long long)cnt;
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
         // alpha (C8): recomputed only when a target crosses into the next Q-quantum
         int64_t q_next = -1;
         float alpha = 0.f;
 
-        int samp_hi = nk < kSampGrp ? nk : kSampGrp;
-        if (K > 0) sample_group(p, 0, samp_hi, c0, kid, kinfo, negs, PV, gshift, lane);
-        __syncwarp();
+        int samp_hi = nk < kSampGrp ? nk : kSampGrp;  // negatives of [0, samp_hi) are in the ring
         int buf = 0;
         int N = gather_list(0, nk, rowid0);
         __syncwarp();
@@ -124,12 +120,16 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 float* dst = r < N ? As + r * RS : Bs + (r - N) * RS;
                 bulk_g2s(dst, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar);
             }
-            // while the rows fly: sample ahead, build the next target's row list, alpha
+            // while the rows fly: fetch negatives ahead, build the next target's row list, alpha.
+            // One cp.async group per target (possibly empty); after iteration m the ring holds
+            // targets up to >= m+9, so waiting for all groups but this one covers target m+1.
             if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kSampGrp) {
                 const int c = nk - samp_hi < kSampGrp ? nk - samp_hi : kSampGrp;
-                sample_group(p, samp_hi, c, c0, kid, kinfo, negs, PV, gshift, lane);
+                fetch_negs(p, rel, samp_hi, c, negs, lane);
                 samp_hi += c;
             }
+            cp_async_commit();
+            cp_async_wait_but_last();
             __syncwarp();
             const int Nn = (m + 1 < nk) ? gather_list(m + 1, nk, rowid0 + (buf ^ 1) * RMAX) : 0;
             const int64_t pi = (int64_t)p.epoch * p.n_local + (pp - p.shard_start);
@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             // tiles of TI = 32/KP1MAX: the TI*KP1MAX partial dots of a tile are finished by ONE
             // butterfly reduce-scatter (lane l ends with dot l = t*KP1MAX + j), σ/G/loss once per
             // lane, G through smem; then per input: ΔOut += G·A (snapshot) and ΔIn over A.
+#ifndef W2V_ABL_NOCOMPUTE
             float2 bq[KP1MAX][CP2], dq[KP1MAX][CP2];
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 #pragma unroll
                 for (int c = 0; c < CP2; ++c)
                     *reinterpret_cast<float2*>(Bs + j * RS + 2 * lane + 64 * c) = dq[j][c];
+#endif  // W2V_ABL_NOCOMPUTE
             fence_proxy_async_smem();
             __syncwarp();
 
@@ -252,7 +254,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             // the next target's gather must see these updates (R11: targets of a chunk are
             // sequential) and the slab must be free: wait for the reductions to complete
+#ifndef W2V_ABL_NOWAIT
             bulk_wait_all();
+#else
+            bulk_wait_read_all();
+#endif
             if (p.deterministic) __threadfence();
             __syncwarp();
             N = Nn;
@@ -316,14 +322,15 @@ const Inst* pick(int D, int K) {
 bool step_supported(int D, int K) { return pick(D, K) != nullptr; }
 
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
-    // [mbarrier 16 B][kid L][kinfo L][rowid 2 x (2w+K+1)][negs 32 x max(K,1)][G tiles x 32]
+    // [mbarrier 8 B | nk 4 B][kid Lp][kinfo Lp][rowid 2 x (2w+K+1)][negs 32 x max(K,1)][G tiles x 32]
     // [slab: KP1MAX B rows + 2w A rows, stride 64*CP2 fp32]
     const Inst* in = pick(D, K);
     if (!in) return 0;
     const int R = 2 * window + K + 1;
     const int TI = 32 / in->kp1;
     const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
-    const size_t ids = 16 + (size_t)(2 * L + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4 + gfl * 4;
+    const int Lp = (L + 3) & ~3;
+    const size_t ids = 16 + (size_t)(2 * Lp + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 127) / 128 * 128;
     if (slab_offset) *slab_offset = (int32_t)off;
     return off + (size_t)(in->kp1 + 2 * window) * 64 * in->cp2 * 4;

@@ -1,5 +1,6 @@
 // hogbatch_common.cuh — device pieces shared by the two fused-step kernels (hogbatch.cu: per-
-// target gather/scatter; hogbatch_win.cu: window-resident rows). Rows a1/a2 of SURVEY.md §8(a).
+// target gather/scatter; hogbatch_win.cu: window-resident rows): reading the batch stream of
+// rows a1/a2 (batch.cu), packed fp32 math, the learning-rate schedule.
 #pragma once
 #include "w2v_device.cuh"
 #include "w2v_internal.h"
@@ -7,8 +8,8 @@
 namespace w2v {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kSampWin = 32;  // ring of sampled targets (negatives staged in smem)
-constexpr int kSampGrp = 8;   // targets sampled together (independent L2 chains in flight)
+constexpr int kSampWin = 32;  // ring of targets whose negatives are staged in smem
+constexpr int kSampGrp = 8;   // targets whose negatives are fetched together (one async group)
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -39,122 +40,29 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     return *reinterpret_cast<float2*>(&d);
 }
 
-// a1 (C2, C4, C5): subsampling of chunk positions [c0, c0+cnt), in-order compaction into
-// kid/kinfo ((offset << 8) | b), debug stream. Returns the number of kept positions.
-__device__ __forceinline__ int compact_chunk(const StepParams& p, int64_t c0, int cnt, int32_t* kid,
-                                             int32_t* kinfo, int lane) {
-    const uint32_t e = (uint32_t)p.epoch;
-    const int window = p.window, KS = p.K > 0 ? p.K : 1;
-    int nk = 0;
-    for (int k0 = 0; k0 < cnt; k0 += 32) {
-        const int k = k0 + lane;
-        bool keep = false;
-        int32_t w = 0;
-        uint32_t u1 = 0;
-        const int64_t pp = c0 + k;
-        if (k < cnt) {
-            w = __ldg(p.ids + (pp - p.ids_base));
-            const U4 r = philox(p.seed, kTagPos, e, (uint64_t)pp, 0u);
-            keep = (uint64_t)r.x < __ldg(p.thr + w);
-            u1 = r.y;
-        }
-        const unsigned m = __ballot_sync(kFull, keep);
-        const int b = 1 + (int)(((uint64_t)u1 * (uint64_t)window) >> 32);
-        if (keep) {
-            const int slot = nk + __popc(m & lanemask_lt());
-            kid[slot] = w;
-            kinfo[slot] = (k << 8) | b;
-        }
-        if (p.dbg_len && k < cnt && pp >= p.dbg_base && pp < p.dbg_base + p.dbg_len) {
-            const int64_t q = pp - p.dbg_base;
-            p.dbg_keep[q] = keep;
-            p.dbg_b[q] = keep ? (uint8_t)b : 0;
-            p.dbg_N[q] = 0;
-            for (int u = 0; u < 2 * window; ++u) p.dbg_ctx[q * 2 * window + u] = -1;
-            for (int u = 0; u < KS; ++u) p.dbg_neg[q * KS + u] = -1;
-        }
-        nk += __popc(m);
-    }
-    return nk;
+// Chunk rel of the launch's batch stream (batch.cu: a1 subsampling + window batching, a2
+// negatives) into the warp's smem: kid / kinfo (Lp ints each, 16-B async copies), the kept count
+// nk, and the negatives of kept targets [0, kSampGrp) into the ring — one cp.async group.
+// Reading past nk (stale slots, or the next chunk's) is harmless: the buffers are padded.
+__device__ __forceinline__ void fetch_negs(const StepParams& p, int64_t rel, int m_lo, int cnt, int32_t* negs,
+                                           int lane) {
+    const int K = p.K;  // K > 0 here, so KS == K and a group of targets is contiguous
+    const int32_t* src = p.bt_neg + (rel * p.Lp + m_lo) * K;
+    int32_t* dst = negs + (m_lo % kSampWin) * K;
+    for (int u = lane; u < cnt * K; u += 32) cp_async4(dst + u, src + u);
 }
-
-// a2 (C7): negatives of kept targets [m_lo, m_lo+cnt) (cnt <= kSampGrp) into the negs ring
-// (slot (m % kSampWin) * KS). Lane d evaluates draw d of every target; the guide-table and
-// prefix loads of all targets are issued together; a ballot then keeps the first K accepted
-// draws of each target (= C7's sequential redraw rule whenever >= K of the first 32 draws are
-// accepted; otherwise a literal sequential fallback on lane 0).
-__device__ __forceinline__ void sample_group(const StepParams& p, int m_lo, int cnt, int64_t c0,
-                                             const int32_t* kid, const int32_t* kinfo, int32_t* negs,
-                                             uint64_t PV, int gshift, int lane) {
-    const uint32_t e = (uint32_t)p.epoch;
-    const int K = p.K, KS = K > 0 ? K : 1;
-    int32_t lo[kSampGrp], hi[kSampGrp], tw[kSampGrp];
-    uint64_t x[kSampGrp];
-#pragma unroll
-    for (int t = 0; t < kSampGrp; ++t) {
-        lo[t] = hi[t] = 0;
-        tw[t] = -1;
-        x[t] = 0;
-        if (t < cnt) {
-            const int64_t pp = c0 + (kinfo[m_lo + t] >> 8);
-            tw[t] = kid[m_lo + t];
-            const U4 r = philox(p.seed, kTagNeg, e, (uint64_t)pp, (uint32_t)(lane >> 1));
-            const uint64_t u = (lane & 1) ? (((uint64_t)r.w << 32) | r.z) : (((uint64_t)r.y << 32) | r.x);
-            x[t] = __umul64hi(u, PV);
-            const uint64_t kb = x[t] >> gshift;
-            lo[t] = __ldg(p.G + kb);
-            hi[t] = __ldg(p.G + kb + 1);
-        }
+__device__ __forceinline__ void load_chunk(const StepParams& p, int64_t rel, int32_t* kid, int32_t* kinfo,
+                                           int32_t* nk_s, int32_t* negs, int lane) {
+    const int q = p.Lp >> 2;
+    const int4* sk = reinterpret_cast<const int4*>(p.bt_kid + rel * p.Lp);
+    const int4* si = reinterpret_cast<const int4*>(p.bt_kinfo + rel * p.Lp);
+    for (int i = lane; i < q; i += 32) {
+        cp_async16(kid + 4 * i, sk + i);
+        cp_async16(kinfo + 4 * i, si + i);
     }
-    for (;;) {  // batched binary search: smallest w in [lo,hi] with P[w+1] > x (C3)
-        bool act = false;
-        int32_t mid[kSampGrp];
-        uint64_t pv[kSampGrp];
-#pragma unroll
-        for (int t = 0; t < kSampGrp; ++t) {
-            mid[t] = lo[t] + ((hi[t] - lo[t]) >> 1);
-            pv[t] = 0;
-            if (lo[t] < hi[t]) {
-                pv[t] = __ldg(p.P + mid[t] + 1);
-                act = true;
-            }
-        }
-        if (!__any_sync(kFull, act)) break;
-#pragma unroll
-        for (int t = 0; t < kSampGrp; ++t)
-            if (lo[t] < hi[t]) {
-                if (pv[t] > x[t]) hi[t] = mid[t];
-                else lo[t] = mid[t] + 1;
-            }
-    }
-#pragma unroll
-    for (int t = 0; t < kSampGrp; ++t) {
-        if (t >= cnt) break;
-        int32_t* out = negs + ((m_lo + t) % kSampWin) * KS;
-        const bool acc = (lo[t] != tw[t]) || p.allow_tn;
-        const unsigned am = __ballot_sync(kFull, acc);
-        if (__popc(am) >= K) {
-            const int rank = __popc(am & lanemask_lt());
-            if (acc && rank < K) out[rank] = lo[t];
-        } else if (lane == 0) {
-            const int64_t pp = c0 + (kinfo[m_lo + t] >> 8);
-            uint32_t d = 0;
-            for (int k = 0; k < K; ++k) {
-                int32_t y = (int32_t)((tw[t] + 1) % p.V);
-                for (int tries = 0; tries < 100; ++tries, ++d) {
-                    const U4 rr = philox(p.seed, kTagNeg, e, (uint64_t)pp, d >> 1);
-                    const uint64_t uu = (d & 1) ? (((uint64_t)rr.w << 32) | rr.z) : (((uint64_t)rr.y << 32) | rr.x);
-                    const int32_t z = invcdf_guided(p.P, p.G, gshift, __umul64hi(uu, PV));
-                    if (z != tw[t] || p.allow_tn) {
-                        y = z;
-                        ++d;
-                        break;
-                    }
-                }
-                out[k] = y;
-            }
-        }
-    }
+    if (lane == 0) cp_async4(nk_s, p.bt_nk + rel);
+    if (p.K > 0) fetch_negs(p, rel, 0, kSampGrp, negs, lane);
+    cp_async_commit();
 }
 
 // C8: alpha for rank-local progress pi (quantised by Q), fp64, rounded to fp32

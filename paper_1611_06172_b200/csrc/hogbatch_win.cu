@@ -44,9 +44,10 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
 
     uint64_t* mbarA = reinterpret_cast<uint64_t*>(wbase);  // window entries
     uint64_t* mbarB = mbarA + 1;                           // [2] target/negative buffers
+    int32_t* nk_s = reinterpret_cast<int32_t*>(wbase + 24);  // kept count of the chunk
     int32_t* kid = reinterpret_cast<int32_t*>(wbase + 32);
-    int32_t* kinfo = kid + p.L;
-    int32_t* pslot = kinfo + p.L;      // slot of kept position (valid while in the window)
+    int32_t* kinfo = kid + p.Lp;
+    int32_t* pslot = kinfo + p.Lp;     // slot of kept position (valid while in the window)
     int32_t* slot_id = pslot + p.L;    // [S]
     int32_t* slot_ref = slot_id + S;   // [S]
     int32_t* negs = slot_ref + S;      // [kSampWin][KS]
@@ -57,8 +58,6 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
     float* acc = val + S * RS;                                      // [S][RS]
     float* Bb = acc + S * RS;                                       // [2][KP1MAX][RS]
 
-    const uint64_t PV = p.info->PV;
-    const int gshift = p.info->gshift;
     const int64_t shard_end = p.shard_start + p.n_local;
 
     if (lane == 0) {
@@ -147,14 +146,16 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         const int cnt = (int)(c1 - c0);
         if (cnt <= 0) continue;
 
-        // ---------------- a1: subsampling + compaction + window
-        const int nk = compact_chunk(p, c0, cnt, kid, kinfo, lane);
-        if (lane == 0) st_words += (unsigned long long)cnt;
+        // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
+        const int64_t rel = s - p.chunk_lo;
+        load_chunk(p, rel, kid, kinfo, nk_s, negs, lane);
+        cp_async_wait_all();
         __syncwarp();
+        const int nk = *nk_s;
+        if (lane == 0) st_words += (unsigned long long)cnt;
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
-        int samp_hi = nk < kSampGrp ? nk : kSampGrp;
-        if (K > 0) sample_group(p, 0, samp_hi, c0, kid, kinfo, negs, PV, gshift, lane);
+        int samp_hi = nk < kSampGrp ? nk : kSampGrp;  // negatives of [0, samp_hi) are in the ring
         // every gather below must see all of this warp's earlier reductions
         bulk_wait_all();
         pend_exit = -1;
@@ -194,12 +195,16 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
                 }
             }
             // ---------------- prefetch for target m+1 (overlaps this target's compute)
+            // (one cp.async group per target; after iteration m the ring holds targets up to
+            // >= m+10, so waiting for all groups but this one covers target m+1)
             if (K > 0 && samp_hi < nk && samp_hi - (m + 2) < kSampGrp) {
                 const int c = nk - samp_hi < kSampGrp ? nk - samp_hi : kSampGrp;
-                sample_group(p, samp_hi, c, c0, kid, kinfo, negs, PV, gshift, lane);
+                fetch_negs(p, rel, samp_hi, c, negs, lane);
                 samp_hi += c;
-                __syncwarp();
             }
+            cp_async_commit();
+            cp_async_wait_but_last();
+            __syncwarp();
             // Sources of earlier reductions must be read before Bp / freed slots are reused, and
             // every group but target m-1's must be complete; a gather that touches a row still in
             // target m-1's group (same M_out id, or the M_in row it wrote back) waits for it.
@@ -419,7 +424,8 @@ size_t win_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     const int P2 = in->kp1 <= 2 ? 2 : in->kp1 <= 4 ? 4 : in->kp1 <= 8 ? 8 : in->kp1 <= 16 ? 16 : 32;
     const int TI = 32 / P2;
     const int tiles = (2 * window + TI - 1) / TI;
-    const size_t ints = (size_t)3 * L + 2 * S + kSampWin * (K > 0 ? K : 1) + 2 * in->kp1 + 2 * window;
+    const int Lp = (L + 3) & ~3;
+    const size_t ints = (size_t)2 * Lp + L + 2 * S + kSampWin * (K > 0 ? K : 1) + 2 * in->kp1 + 2 * window;
     const size_t head = 32 + ints * 4 + (size_t)tiles * 32 * 4;
     const size_t off = (head + 127) / 128 * 128;
     if (slab_offset) *slab_offset = (int32_t)off;

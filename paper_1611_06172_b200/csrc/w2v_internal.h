@@ -45,6 +45,12 @@ struct StepParams {
     int32_t *dbg_ctx, *dbg_neg;
     int32_t warp_bytes;   // dynamic shared memory per warp
     int32_t slab_offset;  // byte offset of the row slab inside a warp's region
+    // batch stream of the launch range (batch.cu), rel = chunk - chunk_lo, Lp = L rounded to 4
+    int32_t Lp;
+    int32_t* bt_nk;       // [chunks]          kept positions per chunk
+    int32_t* bt_kid;      // [chunks][Lp]      kept words, corpus order
+    int32_t* bt_kinfo;    // [chunks][Lp]      (offset << 8) | b
+    int32_t* bt_neg;      // [chunks][Lp][KS]  shared negatives of each kept target
 };
 
 // setup.cu
@@ -54,6 +60,9 @@ cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T
                           uint64_t* P, uint64_t* scratch, int32_t* G, int gbits, SetupInfo* info, cudaStream_t st,
                           int* launches);
 cudaError_t launch_init(float* M, int64_t V, int32_t D, uint64_t seed, int sms, cudaStream_t st);
+
+// batch.cu (a1 subsampling + window batching, a2 negative sampler)
+cudaError_t launch_batch(const StepParams& p, int sms, cudaStream_t st);
 
 // hogbatch_win.cu (window-resident rows; window <= 15)
 size_t win_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
