@@ -218,10 +218,10 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         achieved = last["bytes_row"] / (last["ms_step"] / 1e3) / 1e9   # GB/s, algorithmic bytes
-        traffic = None
+        traffic = None   # DRAM bytes per launch (ncu --set full capture, profiles/), scaled to this launch size
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("dram_bytes_per_word") * n_local / max(last["step_launches"], 1)
         out = {
             "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

@@ -52,6 +52,8 @@ typedef struct {
     int64_t kernel;          /* fused-step kernel of the last w2v_train: 1 rows, 2 window        */
     double  ms_batch;        /* ... of which the a1/a2 batch kernel (subsampling, windows,
                                 negatives; batch.cu), ms — not included in ms_step              */
+    int64_t l2_window_bytes; /* a8: bytes of the hot-row prefix under the persisting-L2 window  */
+    int64_t l2_carve_bytes;  /* a8: persisting-L2 carve-out set for the last w2v_train (0 = off) */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").

@@ -83,7 +83,12 @@ struct Ctx {
     int64_t Q = 10000;
     int allow_tn = 0;
     int64_t dbg_base = 0, dbg_len = 0;
-    int l2_persist = 1;
+    int l2_persist = 0;          // persisting-L2 window (measured harmful: the bulk copies ignore it)
+    int l2_hint = 1;             // a8 cache-policy hints on the row copies (StepParams::l2_hint)
+    int64_t l2_hot_rows = -1;    // hot prefix for the hints (-1 = auto)
+    int64_t l2_window_rows = 0;  // hot-prefix rows under the persisting window (0 = auto)
+    int64_t l2_carve_mb = 0;     // persisting-L2 carve-out, MB (0 = device maximum)
+    int64_t l2_hit_pct = 100;    // hitRatio of the window, percent
     int ctas_per_sm = 0;
     int32_t epochs_total = 0;
     int64_t launch_words = 1ll << 26;
@@ -114,6 +119,7 @@ struct Ctx {
     ncclComm_t comm = nullptr;
     // stats
     w2v_stats_t st{};
+
 } g;
 
 void free_bt() {
@@ -255,6 +261,11 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "debug_base") { if (v < 0) return fail(W2V_EINVAL, "debug_base must be >= 0"); g.dbg_base = v; }
     else if (k == "debug_len") { if (v < 0) return fail(W2V_EINVAL, "debug_len must be >= 0"); g.dbg_len = v; }
     else if (k == "l2_persist") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "l2_persist must be 0/1"); g.l2_persist = (int)v; }
+    else if (k == "l2_hint") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "l2_hint out of [0,3]"); g.l2_hint = (int)v; }
+    else if (k == "l2_hot_rows") { if (v < -1) return fail(W2V_EINVAL, "l2_hot_rows must be >= -1"); g.l2_hot_rows = v; }
+    else if (k == "l2_window_rows") { if (v < 0) return fail(W2V_EINVAL, "l2_window_rows must be >= 0"); g.l2_window_rows = v; }
+    else if (k == "l2_carve_mb") { if (v < 0) return fail(W2V_EINVAL, "l2_carve_mb must be >= 0"); g.l2_carve_mb = v; }
+    else if (k == "l2_hit_pct") { if (v < 1 || v > 100) return fail(W2V_EINVAL, "l2_hit_pct out of [1,100]"); g.l2_hit_pct = v; }
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "kernel") { if (v < 0 || v > 2) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows) or 2 (window)"); g.kernel = (int)v; }
@@ -361,22 +372,28 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     }
     // ---- a8: persisting-L2 window over the hot prefix rows of [M_in|M_out]
     bool window_set = false;
+    g.st.l2_window_bytes = g.st.l2_carve_bytes = 0;
     if (g.l2_persist && g.mode == 0) {
         int maxp = 0, maxwin = 0;
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g.device);
         cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g.device);
         if (maxp > 0 && maxwin > 0) {
-            size_t bytes = std::min<size_t>((size_t)maxp, (size_t)maxwin);
-            bytes = std::min<size_t>(bytes, (size_t)g.V * 2 * g.D * 4);
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess) {
+            const size_t rowb = (size_t)2 * g.D * 4;
+            size_t carve = g.l2_carve_mb > 0 ? std::min<size_t>((size_t)g.l2_carve_mb << 20, (size_t)maxp) : (size_t)maxp;
+            size_t bytes = g.l2_window_rows > 0 ? (size_t)g.l2_window_rows * rowb : carve;
+            bytes = std::min<size_t>(bytes, (size_t)maxwin);
+            bytes = std::min<size_t>(bytes, (size_t)g.V * rowb);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
                 cudaStreamAttrValue a{};
                 a.accessPolicyWindow.base_ptr = g.M;
                 a.accessPolicyWindow.num_bytes = bytes;
-                a.accessPolicyWindow.hitRatio = 1.0f;
+                a.accessPolicyWindow.hitRatio = (float)g.l2_hit_pct / 100.0f;
                 a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
                 a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
                 window_set = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess;
             }
+            g.st.l2_window_bytes = window_set ? (int64_t)bytes : 0;
+            g.st.l2_carve_bytes = window_set ? (int64_t)carve : 0;
         }
         cudaGetLastError();
     }
@@ -396,6 +413,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.thr = g.thr; p.P = g.P; p.G = g.G; p.info = g.info; p.M = g.M;
     p.chunk_ctr = g.chunk_ctr; p.stats = g.dstats;
     p.loss_tail_from = g.loss_tail_from;
+    p.l2_hint = g.l2_hint;
+    p.hot_rows = g.l2_hot_rows >= 0 ? g.l2_hot_rows : (int64_t)(64ll << 20) / ((int64_t)2 * g.D * 4);
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
     // kernel choice: window-resident rows when the window fits, else per-target
@@ -473,6 +492,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     DevStats hs{};
     CU(cudaMemcpyAsync(&hs, g.dstats, sizeof hs, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    step_phase_report();
     if (window_set) {
         cudaStreamAttrValue a{};
         a.accessPolicyWindow.num_bytes = 0;

@@ -27,6 +27,15 @@
 
 namespace w2v {
 
+#if defined(W2V_PHASE_TIMING)
+// (experiment) cycles per phase summed over warps: chunk load, gather issue->landed, compute,
+// scatter issue->complete, targets
+__device__ unsigned long long g_phase[8];
+#define W2V_T(...) __VA_ARGS__
+#else
+#define W2V_T(...)
+#endif
+
 namespace {
 
 #ifndef W2V_MINB
@@ -57,12 +66,15 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
     const int64_t shard_end = p.shard_start + p.n_local;
 
+    const uint64_t pol_hot = (p.l2_hint & 1) ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_cold = (p.l2_hint & 2) ? policy_evict_first() : policy_evict_normal();
     if (lane == 0) mbar_init(mbar, 1);
     for (int i = lane; i < (KP1MAX + 2 * window) * RS / 4; i += 32)
         reinterpret_cast<float4*>(Bs)[i] = make_float4(0.f, 0.f, 0.f, 0.f);  // padding stays 0
     __syncwarp();
     uint32_t phase = 0;
 
+    W2V_T(unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0, st_tail_pairs = 0;
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
@@ -93,9 +105,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
         // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
         const int64_t rel = s - p.chunk_lo;
+        W2V_T(long long t0 = clock64();)
         load_chunk(p, rel, kid, kinfo, nk_s, negs, lane);
         cp_async_wait_all();
         __syncwarp();
+        W2V_T(ph[0] += clock64() - t0;)
         const int nk = *nk_s;
         if (lane == 0) st_words += (unsigned long long)cnt;
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
@@ -113,12 +127,22 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             const int R = N + KP1;
             const int64_t pp = c0 + (kinfo[m] >> 8);
             // ---------------- a3: gather the snapshot rows (one bulk copy per row)
+            W2V_T(long long t1 = clock64();)
+#ifndef W2V_ABL_NOGATHER
             if (lane == 0) mbar_arrive_expect_tx(mbar, (uint32_t)R * rowbytes);
+#else
+            if (lane == 0) mbar_arrive_expect_tx(mbar, 0u);
+#endif
             __syncwarp();
             for (int r = lane; r < R; r += 32) {
                 const int32_t id = rowid[r];
                 float* dst = r < N ? As + r * RS : Bs + (r - N) * RS;
-                bulk_g2s(dst, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar);
+#ifndef W2V_ABL_NOGATHER
+                bulk_g2s_hint(dst, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar,
+                              id < p.hot_rows ? pol_hot : pol_cold);
+#else
+                (void)dst; (void)id;
+#endif
             }
             // while the rows fly: fetch negatives ahead, build the next target's row list, alpha.
             // One cp.async group per target (possibly empty); after iteration m the ring holds
@@ -138,8 +162,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 q_next = (qi + 1) * p.Q;
                 alpha = alpha_at(p, qi);
             }
+            W2V_T(long long t2 = clock64(); ph[5] += t2 - t1;)
             mbar_wait(mbar, phase);
             phase ^= 1u;
+            W2V_T(long long t3 = clock64(); ph[1] += t3 - t1;)
 
             // ---------------- a4-a6: C = A·Bᵀ, E, G, ΔIn (over A), ΔOut (registers, then over B)
             // Rows are padded to RS floats and B to KP1MAX rows with zeros (never written by
@@ -228,11 +254,20 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             fence_proxy_async_smem();
             __syncwarp();
 
+            W2V_T(long long t4 = clock64(); ph[2] += t4 - t3;)
             // ---------------- a7: Hogwild scatter-add, one bulk fp32 reduction per row at L2
             for (int r = lane; r < R; r += 32) {
                 const int32_t id = rowid[r];
                 const float* src = r < N ? As + r * RS : Bs + (r - N) * RS;
-                bulk_red_add_s2g(p.M + (size_t)id * 2 * D + (r < N ? 0 : D), src, rowbytes);
+#if defined(W2V_ABL_NOHOT)
+                if (id < W2V_ABL_NOHOT) continue;
+#endif
+#ifndef W2V_ABL_NOSCATTER
+                bulk_red_add_s2g_hint(p.M + (size_t)id * 2 * D + (r < N ? 0 : D), src, rowbytes,
+                                      id < p.hot_rows ? pol_hot : pol_cold);
+#else
+                (void)src; (void)id;
+#endif
             }
             bulk_commit();
             st_loss += (double)st_loss_f;   // per-target partial (<= N terms) into fp64 (C11)
@@ -254,13 +289,14 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             // the next target's gather must see these updates (R11: targets of a chunk are
             // sequential) and the slab must be free: wait for the reductions to complete
-#ifndef W2V_ABL_NOWAIT
+#if !defined(W2V_ABL_NOWAIT)
             bulk_wait_all();
 #else
             bulk_wait_read_all();
 #endif
             if (p.deterministic) __threadfence();
             __syncwarp();
+            W2V_T(ph[3] += clock64() - t4; ph[4] += 1;)
             N = Nn;
             buf ^= 1;
         }
@@ -272,6 +308,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         st_loss += __shfl_xor_sync(kFull, st_loss, o);
         st_tail += __shfl_xor_sync(kFull, st_tail, o);
     }
+    W2V_T(if (lane == 0) for (int i = 0; i < 8; ++i) atomicAdd(&g_phase[i], ph[i]);)
     if (lane == 0) {
         atomicAdd(&p.stats->words, st_words);
         atomicAdd(&p.stats->targets, st_targets);
@@ -320,6 +357,18 @@ const Inst* pick(int D, int K) {
 }  // namespace
 
 bool step_supported(int D, int K) { return pick(D, K) != nullptr; }
+
+void step_phase_report() {
+#if defined(W2V_PHASE_TIMING)
+    unsigned long long h[8];
+    cudaMemcpyFromSymbol(h, g_phase, sizeof h);
+    const double T = h[4] ? (double)h[4] : 1.0;
+    fprintf(stderr, "[phase] per target (cycles): chunk-load %.0f  gather->landed %.0f (issue+prep %.0f)  compute %.0f  scatter->done %.0f  targets %llu\n",
+            h[0] / T, h[1] / T, h[5] / T, h[2] / T, h[3] / T, h[4]);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase, z, sizeof z);
+#endif
+}
 
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     // [mbarrier 8 B | nk 4 B][kid Lp][kinfo Lp][rowid 2 x (2w+K+1)][negs 32 x max(K,1)][G tiles x 32]

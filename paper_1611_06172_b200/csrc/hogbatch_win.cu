@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
 
     const int64_t shard_end = p.shard_start + p.n_local;
 
+    const uint64_t pol_hot = (p.l2_hint & 1) ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_cold = (p.l2_hint & 2) ? policy_evict_first() : policy_evict_normal();
     if (lane == 0) {
         mbar_init(mbarA, 1);
         mbar_init(mbarB, 1);
@@ -106,7 +108,8 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         if (lane == 0) mbar_arrive_expect_tx(mbarA, bytesA);
         __syncwarp();
         if ((newslots >> lane) & 1u)
-            bulk_g2s(val + lane * RS, p.M + (size_t)slot_id[lane] * 2 * D, rowbytes, mbarA);
+            bulk_g2s_hint(val + lane * RS, p.M + (size_t)slot_id[lane] * 2 * D, rowbytes, mbarA,
+                          slot_id[lane] < p.hot_rows ? pol_hot : pol_cold);
         newslots = 0;
         bytesA = 0;
     };
@@ -116,7 +119,9 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         __syncwarp();
         if (lane == 0) {
             slot_ref[s] = ref;
-            if (ref == 0) bulk_red_add_s2g(p.M + (size_t)slot_id[s] * 2 * D, acc + s * RS, rowbytes);
+            if (ref == 0)
+                bulk_red_add_s2g_hint(p.M + (size_t)slot_id[s] * 2 * D, acc + s * RS, rowbytes,
+                                      slot_id[s] < p.hot_rows ? pol_hot : pol_cold);
         }
         if (ref == 0) {
             freem |= 1u << s;
@@ -132,7 +137,9 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         __syncwarp();
         if (lane == 0) mbar_arrive_expect_tx(mbarB + buf, (uint32_t)KP1 * rowbytes);
         __syncwarp();
-        if (lane < KP1) bulk_g2s(Bb + (buf * KP1MAX + lane) * RS, p.M + (size_t)ids[lane] * 2 * D + D, rowbytes, mbarB + buf);
+        if (lane < KP1)
+            bulk_g2s_hint(Bb + (buf * KP1MAX + lane) * RS, p.M + (size_t)ids[lane] * 2 * D + D, rowbytes, mbarB + buf,
+                          ids[lane] < p.hot_rows ? pol_hot : pol_cold);
     };
 
     for (;;) {
@@ -341,7 +348,9 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
             __syncwarp();
 
             // ---------------- a7: ΔOut rows now; position m-w leaves the window
-            if (lane < KP1) bulk_red_add_s2g(p.M + (size_t)bidc[lane] * 2 * D + D, Bc + lane * RS, rowbytes);
+            if (lane < KP1)
+                bulk_red_add_s2g_hint(p.M + (size_t)bidc[lane] * 2 * D + D, Bc + lane * RS, rowbytes,
+                                      bidc[lane] < p.hot_rows ? pol_hot : pol_cold);
             if (m - w >= 0) leave(m - w);
             bulk_commit();
 

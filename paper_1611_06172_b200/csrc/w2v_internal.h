@@ -51,6 +51,10 @@ struct StepParams {
     int32_t* bt_kid;      // [chunks][Lp]      kept words, corpus order
     int32_t* bt_kinfo;    // [chunks][Lp]      (offset << 8) | b
     int32_t* bt_neg;      // [chunks][Lp][KS]  shared negatives of each kept target
+    // a8: L2 eviction-priority hints on the row copies: rows with id < hot_rows (the Zipf-hot
+    // prefix) get evict_last if l2_hint & 1; the others evict_first if l2_hint & 2
+    int64_t hot_rows;
+    int32_t l2_hint;
 };
 
 // setup.cu
@@ -74,5 +78,6 @@ bool step_supported(int D, int K);
 cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st);
 int step_max_ctas_per_sm(const StepParams& p);
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
+void step_phase_report();  // (experiment builds with W2V_PHASE_TIMING) prints per-phase cycles
 
 }  // namespace w2v

@@ -25,6 +25,16 @@ VARIANTS = {
     "nocompute": ["-DW2V_ABL_NOCOMPUTE"],
     "nowait": ["-DW2V_ABL_NOWAIT"],
     "nocompute_nowait": ["-DW2V_ABL_NOCOMPUTE", "-DW2V_ABL_NOWAIT"],
+    "nogather": ["-DW2V_ABL_NOGATHER"],
+    "g_ldgsts": ["-DW2V_GATHER_LDGSTS"],
+    "s_red": ["-DW2V_SCATTER_RED"],
+    "s_red_fence": ["-DW2V_SCATTER_RED", "-DW2V_RED_FENCE"],
+    "ldgsts_red_fence": ["-DW2V_GATHER_LDGSTS", "-DW2V_SCATTER_RED", "-DW2V_RED_FENCE"],
+    "noscatter": ["-DW2V_ABL_NOSCATTER"],
+    "phase": ["-DW2V_PHASE_TIMING"],
+    "nohot16": ["-DW2V_ABL_NOHOT=16"],
+    "nohot256": ["-DW2V_ABL_NOHOT=256"],
+    "nohot4096": ["-DW2V_ABL_NOHOT=4096"],
 }
 
 
@@ -35,7 +45,7 @@ def build(names):
         print(n, _build.build(out=os.path.join(OUT, f"libw2v_{n}.so"), extra=VARIANTS[n]), flush=True)
 
 
-def one(so, tokens, opts, reps):
+def one(so, tokens, opts, reps, vmod=0):
     import numpy as np  # noqa: F401
     import torch
     os.environ["W2V_LIBRARY"] = so
@@ -44,8 +54,12 @@ def one(so, tokens, opts, reps):
     cfg = inputs.CONFIGS[3]
     host = torch.empty(tokens, dtype=torch.int32, pin_memory=True)
     cfg.corpus().tokens(0, tokens, out=host.numpy())
+    V = cfg.V
+    if vmod:  # (experiment) fold the vocabulary so the whole model fits in L2
+        host.remainder_(vmod)
+        V = vmod
     dev = host.cuda()
-    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.init(V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     for k, v in opts.items():
         w2v.set_option(k, v)
@@ -57,18 +71,22 @@ def one(so, tokens, opts, reps):
             best = st
     w2v.finalize()
     return {"words_per_s": tokens / (best["ms_step"] / 1e3), "ms_step": best["ms_step"],
-            "row_GBps": best["bytes_row"] / (best["ms_step"] / 1e3) / 1e9, "ms_batch": best["ms_batch"]}
+            "row_GBps": best["bytes_row"] / (best["ms_step"] / 1e3) / 1e9, "ms_batch": best["ms_batch"],
+            "l2_window_MB": best["l2_window_bytes"] / 2**20, "l2_carve_MB": best["l2_carve_bytes"] / 2**20}
 
 
-def run(names, tokens, sweeps, reps):
+def run(names, tokens, sweeps, reps, vmod=0):
     for n in names:
         so = os.path.join(OUT, f"libw2v_{n}.so")
         for opts in sweeps:
             code = (f"import sys, json; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.dirname(__file__)!r});"
-                    f"import ablate; print(json.dumps(ablate.one({so!r}, {tokens}, {opts!r}, {reps})))")
+                    f"import ablate; print(json.dumps(ablate.one({so!r}, {tokens}, {opts!r}, {reps}, {vmod})))")
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
             line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
             print(json.dumps({"variant": n, "opts": opts, "result": line}), flush=True)
+            for ln in r.stderr.splitlines():
+                if ln.startswith("[phase]"):
+                    print("   ", ln, flush=True)
 
 
 if __name__ == "__main__":
@@ -78,10 +96,14 @@ if __name__ == "__main__":
     ap.add_argument("--tokens", type=int, default=1 << 27)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--occ", default="0", help="comma list of ctas_per_sm values (0 = max)")
+    ap.add_argument("--vmod", type=int, default=0, help="experiment: ids %% vmod, V = vmod")
+    ap.add_argument("--opts", default="", help="extra option sets: 'k=v,k=v;k=v' (each ';' part is one run)")
     a = ap.parse_args()
     names = a.variants.split(",")
     if a.what == "build":
         build(names)
     else:
         sweeps = [{"ctas_per_sm": int(x)} if int(x) else {} for x in a.occ.split(",")]
-        run(names, a.tokens, sweeps, a.reps)
+        if a.opts:
+            sweeps = [dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in part.split(",")) for part in a.opts.split(";")]
+        run(names, a.tokens, sweeps, a.reps, a.vmod)

@@ -4,9 +4,12 @@ import os
 import subprocess
 import sys
 
+# kernel filter for multi-kernel reports (the step kernel by default)
+KFILT = os.environ.get("W2V_NCU_KERNEL", "regex:hogbatch_step")
+
 
 def main(rep, top=40):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    out = subprocess.run(["ncu", "-i", rep, "-k", KFILT, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout.splitlines()
     rows = list(csv.reader(out))
     hdr = None

@@ -1,10 +1,14 @@
 """Executed-instruction mix by SASS opcode from an ncu report's source page."""
 import collections
 import csv
+import os
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "sass"],
+# kernel filter for multi-kernel reports (the step kernel by default)
+KFILT = os.environ.get("W2V_NCU_KERNEL", "regex:hogbatch_step")
+
+out = subprocess.run(["ncu", "-i", sys.argv[1], "-k", KFILT, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 hdr = None

@@ -72,8 +72,9 @@ def main(tag, csv_path, rep, bench_log):
                                capture_output=True, text=True).stdout
     with open(os.path.join(ROOT, "profiles", f"{tag}_hogbatch_step_ncu.md"), "w") as f:
         f.write(f"# {tag}: `ncu --set full` of one hogbatch_step launch ({words} raw words of cfg3)\n\n")
-        f.write("Command: `ncu --set full --clock-control none --import-source on -k regex:hogbatch_step -s 5 -c 1 "
-                "python bench.py --steps 1 --warmup 1 --no-cpu-baseline` (after the same command exited 0).\n\n")
+        cmd = os.environ.get("W2V_PROFILED_CMD", "ncu --set full --clock-control none --import-source on "
+                             "-k regex:hogbatch_step -s 5 -c 1 python bench.py --steps 1 --warmup 1 --no-cpu-baseline")
+        f.write(f"Command: `{cmd}` (after the same command exited 0).\n\n")
         f.write("| metric | unit | value |\n|---|---|---|\n")
         for k, (v, u) in s.items():
             f.write(f"| {k} | {u} | {v} |\n")
