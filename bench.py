@@ -164,6 +164,7 @@ def run_ours(args):
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", SYNC_P)
     w2v.set_option("kernel", args.kernel)
+    w2v.set_option("algorithm", 1 if args.algorithm == "alg1" else 0)
     stream = torch.cuda.current_stream()
     w2v.set_stream(stream.cuda_stream)
     if world > 1:
@@ -231,9 +232,11 @@ def run_ours(args):
                        "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": SYNC_P if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
-                       "mode": "hogwild", "kernel": {1: "rows", 2: "window"}.get(last["kernel"])},
+                       "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "alg1"}.get(last["kernel"]),
+                       "algorithm": "hogbatch" if args.algorithm == "hogbatch" else "alg1 (PAPER.md:37-63, level-1 baseline)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "hogbatch_step",
+                         "frac": achieved / peak, "traffic": traffic if args.algorithm == "hogbatch" else None,
+                         "kernel": "hogbatch_step" if args.algorithm == "hogbatch" else "alg1",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
                          "row_bytes_per_word": last["bytes_row"] / n_local,
@@ -264,6 +267,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 per-target rows, 2 window-resident rows")
     ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
+    ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
+                    help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -77,7 +77,18 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "allow_target_negative" 0/1 (R2; default 0)
  *  "debug_base","debug_len" record the batch stream (C5-C7) for global positions
  *                          [base, base+len) during the next w2v_train (len 0 = off)
- *  "l2_persist"            0/1 persisting-L2 access window over the hot-row prefix (a8; default 1)
+ *  "algorithm"             0 = HogBatch (default), 1 = Algorithm 1, the
+ *                          "original" level-1 SGNS update: per-input negatives
+ *                          on the A1NEG stream, one dot + immediate update per (input, output)
+ *                          pair, N(K+1)+N row updates per target
+ *  "l2_hint"               a8 L2 eviction-priority hints on the row copies: bit 0 = evict_last
+ *                          on the hot prefix, bit 1 = evict_first on the other rows (default 1)
+ *  "l2_hot_rows"           hot prefix for l2_hint (-1 = the rows that fit 64 MB; default -1)
+ *  "l2_persist"            0/1 persisting-L2 access-policy window over the hot-row prefix
+ *                          (default 0: measured harmful on B200, the bulk copies ignore it and
+ *                          the carve-out only shrinks L2; profiles/r01_ablations.md §2)
+ *  "l2_window_rows", "l2_carve_mb", "l2_hit_pct"  that window's rows (0 = carve-out size),
+ *                          carve-out in MB (0 = device maximum) and hitRatio in percent
  *  "ctas_per_sm"           0 = occupancy maximum (default), else that many 1-warp CTAs per SM
  *  "launch_words"          raw words per hogbatch_step launch (>=1; default 2^26): bounds a
  *                          launch's duration; results do not depend on it in deterministic mode
@@ -126,6 +137,12 @@ int w2v_get_stats(w2v_stats_t* out);
  * int32[len][2*window] (-1 padded), neg int32[len][max(K,1)] (-1 padded). Host or device;
  * any pointer may be NULL. ESTATE if nothing was recorded. */
 int w2v_debug_batches(uint8_t* keep, uint8_t* b, uint8_t* N, int32_t* ctx, int32_t* neg);
+
+/* Algorithm 1 only (option "algorithm" = 1): copy the per-input negatives recorded by the last
+ * w2v_train for [debug_base, debug_base+debug_len): int32[len][2*window][max(K,1)], entry
+ * [q][i][k] = the k-th negative of input i of the target at position base+q (Alg.1 l.10),
+ * -1 padded. Host or device. ESTATE if nothing was recorded. */
+int w2v_debug_alg1_negatives(int32_t* neg);
 
 /* Data-parallel bootstrap (C13). Rank 0 creates a 128-byte NCCL unique id; the caller
  * broadcasts it (torch.distributed) and every rank calls w2v_dist_init. world == 1 with a NULL id

@@ -52,7 +52,7 @@ class OrcDebug(ctypes.Structure):
     _fields_ = [("base", ctypes.c_int64), ("len", ctypes.c_int64),
                 ("keep", ctypes.POINTER(ctypes.c_uint8)), ("b", ctypes.POINTER(ctypes.c_uint8)),
                 ("N", ctypes.POINTER(ctypes.c_uint8)), ("ctx", ctypes.POINTER(ctypes.c_int32)),
-                ("neg", ctypes.POINTER(ctypes.c_int32))]
+                ("neg", ctypes.POINTER(ctypes.c_int32)), ("a1neg", ctypes.POINTER(ctypes.c_int32))]
 
 
 _libs: dict = {}
@@ -212,8 +212,10 @@ class Debug:
         self.N = np.zeros(length, np.uint8)
         self.ctx = np.full((length, 2 * window), -1, np.int32)
         self.neg = np.full((length, max(K, 1)), -1, np.int32)
+        self.a1neg = np.full((length, 2 * window, max(K, 1)), -1, np.int32)  # O-A1 per-input negatives
         self.c = OrcDebug(base, length, _p(self.keep, ctypes.c_uint8), _p(self.b, ctypes.c_uint8),
-                          _p(self.N, ctypes.c_uint8), _p(self.ctx, ctypes.c_int32), _p(self.neg, ctypes.c_int32))
+                          _p(self.N, ctypes.c_uint8), _p(self.ctx, ctypes.c_int32), _p(self.neg, ctypes.c_int32),
+                          _p(self.a1neg, ctypes.c_int32))
 
 
 def make_params(V, D, window, K, alpha0, t, seed, L, epochs, n_global, world=1, lr_quantum=10_000,

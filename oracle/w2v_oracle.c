@@ -296,6 +296,7 @@ typedef struct {
     uint8_t* N;
     int32_t* ctx;
     int32_t* neg;
+    int32_t* a1neg;  /* O-A1 only: the K negatives of each input i, [len][2*window][K] (-1 padded) */
 } orc_debug;
 
 /* Train on global chunks [chunk_lo, chunk_hi) for epoch e (C5-C8, Sec. "Oracle
@@ -336,6 +337,7 @@ int orc_train_range(const orc_params* prm, const uint64_t* thr, const uint64_t* 
                 if (dbg->N) dbg->N[q] = 0;
                 if (dbg->ctx) for (int32_t u = 0; u < W2; ++u) dbg->ctx[q * W2 + u] = -1;
                 if (dbg->neg) for (int32_t u = 0; u < K; ++u) dbg->neg[q * K + u] = -1;
+                if (dbg->a1neg) for (int32_t u = 0; u < W2 * K; ++u) dbg->a1neg[q * W2 * K + u] = -1;
             }
         }
         st->words += c1 - c0;
@@ -398,6 +400,8 @@ int orc_train_range(const orc_params* prm, const uint64_t* thr, const uint64_t* 
                 if (dbg->ctx) for (int32_t u = 0; u < N; ++u) dbg->ctx[q * W2 + u] = ctx[u];
                 if (dbg->neg && prm->algorithm == 0)
                     for (int32_t u = 0; u < K; ++u) dbg->neg[q * K + u] = outs[u + 1];
+                if (dbg->a1neg && prm->algorithm == 1)
+                    for (int32_t u = 0; u < N * K; ++u) dbg->a1neg[q * W2 * K + u] = negs[u];
             }
         }
     }

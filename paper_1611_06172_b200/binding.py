@@ -44,6 +44,7 @@ _lib.w2v_get_embeddings.argtypes = [ctypes.c_int32, _vp]
 _lib.w2v_set_embeddings.argtypes = [ctypes.c_int32, _vp]
 _lib.w2v_get_stats.argtypes = [ctypes.POINTER(Stats)]
 _lib.w2v_debug_batches.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.w2v_debug_alg1_negatives.argtypes = [_vp]
 _lib.w2v_dist_unique_id.argtypes = [_vp]
 _lib.w2v_dist_init.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp]
 _lib.w2v_dist_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
@@ -116,6 +117,10 @@ def get_stats() -> dict:
 
 def debug_batches(keep=None, b=None, N=None, ctx=None, neg=None):
     return _check(_lib.w2v_debug_batches(_ptr(keep), _ptr(b), _ptr(N), _ptr(ctx), _ptr(neg)))
+
+
+def debug_alg1_negatives(neg):
+    return _check(_lib.w2v_debug_alg1_negatives(_ptr(neg)))
 
 
 def dist_unique_id() -> bytes:

@@ -89,12 +89,42 @@ __global__ void __launch_bounds__(32 * kBatchWarps) batch_kernel(const StepParam
                 p.dbg_N[q] = 0;  // the step kernel fills N / ctx / negatives of trained targets
                 for (int u = 0; u < 2 * window; ++u) p.dbg_ctx[q * 2 * window + u] = -1;
                 for (int u = 0; u < KS; ++u) p.dbg_neg[q * KS + u] = -1;
+                if (p.dbg_a1neg)
+                    for (int u = 0; u < 2 * window * KS; ++u) p.dbg_a1neg[q * 2 * window * KS + u] = -1;
             }
             nk += __popc(m);
         }
         if (lane == 0) p.bt_nk[rel] = nk;
         if (nk < 2 || K == 0) continue;  // N = 0 for every kept target iff nk < 2
         __syncwarp();                    // kid / kinfo written by other lanes are visible below
+
+        if (p.algorithm == 1) {
+            // ---- Alg.1 l.10: K negatives per (target m, input i) on the A1NEG stream, draw
+            // counter d restarting at 0 per input, block idx = i << 12 | d >> 1 (C1). One lane
+            // per (m, i) runs C7's redraw rule literally.
+            const int W2 = 2 * window;
+            for (int u = lane; u < nk * W2; u += 32) {
+                const int m = u / W2, i = u - m * W2;
+                const int bm = kinfo[m] & 255;
+                const int lo = m - bm < 0 ? 0 : m - bm, hi = m + bm > nk - 1 ? nk - 1 : m + bm;
+                if (i >= hi - lo) continue;
+                const int64_t pp = c0 + (kinfo[m] >> 8);
+                const int32_t tw = kid[m];
+                int32_t* out = p.bt_neg + ((rel * Lp + m) * W2 + i) * K;
+                uint32_t d = 0;
+                for (int k = 0; k < K; ++k) {
+                    int32_t y = (int32_t)((tw + 1) % p.V);
+                    for (int tries = 0; tries < 100; ++tries, ++d) {
+                        const U4 r = philox(p.seed, kTagA1Neg, e, (uint64_t)pp, ((uint32_t)i << 12) | (d >> 1));
+                        const uint64_t uu = (d & 1) ? (((uint64_t)r.w << 32) | r.z) : (((uint64_t)r.y << 32) | r.x);
+                        const int32_t z = invcdf_guided(p.P, p.G, gshift, __umul64hi(uu, PV));
+                        if (z != tw || p.allow_tn) { y = z; ++d; break; }
+                    }
+                    out[k] = y;
+                }
+            }
+            continue;
+        }
 
         // ---- a2: K negatives per kept target (C7). Lane u handles draw d = u % K of target
         // m = u / K, assuming no rejection before it; a target whose first K draws contain a

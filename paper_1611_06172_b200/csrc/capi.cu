@@ -94,6 +94,7 @@ struct Ctx {
     int64_t launch_words = 1ll << 26;
     int64_t loss_tail_from = INT64_MAX;
     int kernel = 0;  // 0 auto, 1 per-target rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
+    int algorithm = 0;  // 0 HogBatch, 1 Alg.1 (alg1.cu)
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -112,7 +113,7 @@ struct Ctx {
     size_t bt_cap_nk = 0, bt_cap_kid = 0, bt_cap_neg = 0;
     // debug
     uint8_t *dbg_keep = nullptr, *dbg_b = nullptr, *dbg_N = nullptr;
-    int32_t *dbg_ctx = nullptr, *dbg_neg = nullptr;
+    int32_t *dbg_ctx = nullptr, *dbg_neg = nullptr, *dbg_a1neg = nullptr;
     int64_t dbg_rec_len = 0;
     // dist
     int rank = 0, world = 1;
@@ -130,8 +131,9 @@ void free_bt() {
 
 void free_dbg() {
     cudaFree(g.dbg_keep); cudaFree(g.dbg_b); cudaFree(g.dbg_N); cudaFree(g.dbg_ctx); cudaFree(g.dbg_neg);
+    cudaFree(g.dbg_a1neg);
     g.dbg_keep = g.dbg_b = g.dbg_N = nullptr;
-    g.dbg_ctx = g.dbg_neg = nullptr;
+    g.dbg_ctx = g.dbg_neg = g.dbg_a1neg = nullptr;
     g.dbg_rec_len = 0;
 }
 
@@ -268,6 +270,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "l2_hit_pct") { if (v < 1 || v > 100) return fail(W2V_EINVAL, "l2_hit_pct out of [1,100]"); g.l2_hit_pct = v; }
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
+    else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 2) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows) or 2 (window)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
@@ -368,6 +371,10 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         CU(cudaMemsetAsync(g.dbg_N, 0, Lq, st));
         CU(cudaMemsetAsync(g.dbg_ctx, 0xff, (size_t)Lq * 2 * g.window * 4, st));
         CU(cudaMemsetAsync(g.dbg_neg, 0xff, (size_t)Lq * kk * 4, st));
+        if (g.algorithm == 1) {
+            if ((rc = dmalloc((void**)&g.dbg_a1neg, (size_t)Lq * 2 * g.window * kk * 4, "debug Alg.1 negatives"))) return rc;
+            CU(cudaMemsetAsync(g.dbg_a1neg, 0xff, (size_t)Lq * 2 * g.window * kk * 4, st));
+        }
         g.dbg_rec_len = Lq;
     }
     // ---- a8: persisting-L2 window over the hot prefix rows of [M_in|M_out]
@@ -417,6 +424,10 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.hot_rows = g.l2_hot_rows >= 0 ? g.l2_hot_rows : (int64_t)(64ll << 20) / ((int64_t)2 * g.D * 4);
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
+    p.dbg_a1neg = g.dbg_a1neg;
+    p.algorithm = g.algorithm;
+    if (g.algorithm == 1 && !alg1_supported(g.D, g.K))
+        return fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K);
     // kernel choice: window-resident rows when the window fits, else per-target
     int32_t off_win = 0, off_row = 0;
     const size_t wb_win = win_warp_bytes(g.L, g.window, g.K, g.D, &off_win);
@@ -426,28 +437,35 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     if (g.kernel != 2) use_win = false;  // auto = per-target rows (measured faster)
     if (g.kernel == 2 && !use_win)
         return fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
-    const size_t wb = use_win ? wb_win : wb_row;
+    if (g.algorithm == 1) use_win = false;
+    size_t wb = use_win ? wb_win : wb_row;
+    if (g.algorithm == 1) wb = alg1_warp_bytes(g.L);
     p.slab_offset = use_win ? off_win : off_row;
     if (wb == 0 || wb > kSmemMax) return fail(W2V_EINVAL, "w2v_train: per-warp shared memory %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
     p.warp_bytes = (int32_t)wb;
     int ctas = 1;
     if (g.mode == 0) {
-        int occ = use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
+        int occ = g.algorithm == 1 ? alg1_max_ctas_per_sm(p) : use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
         if (occ < 1) return fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per warp)", wb);
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
-    g.st.kernel = use_win ? 2 : 1;
+    g.st.kernel = g.algorithm == 1 ? 3 : use_win ? 2 : 1;
     CU(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
     const int64_t chunk_hi = (shard_start + n + g.L - 1) / g.L;
     // an interval is issued as launches of at most launch_words raw words (bounded kernel
     // duration and batch-stream size); chunks are still claimed in corpus order in each launch
-    const int64_t per = std::max<int64_t>(1, g.launch_words / g.L);
+    int64_t per = std::max<int64_t>(1, g.launch_words / g.L);
     p.Lp = (g.L + 3) & ~3;
+    // negatives per kept slot: K shared (HogBatch) or 2*window*K per-input (Alg.1); Alg.1
+    // launches are shortened so that its larger negative buffer stays <= 1 GiB
+    const int32_t negs_per_slot = g.algorithm == 1 ? 2 * g.window * (g.K > 0 ? g.K : 1) : (g.K > 0 ? g.K : 1);
+    if (g.algorithm == 1)
+        per = std::max<int64_t>(1, std::min<int64_t>(per, (1ll << 30) / ((int64_t)p.Lp * negs_per_slot * 4)));
     {
-        int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, g.K > 0 ? g.K : 1);
+        int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, negs_per_slot);
         if (rc) return rc;
     }
     p.bt_nk = g.bt_nk; p.bt_kid = g.bt_kid; p.bt_kinfo = g.bt_kinfo; p.bt_neg = g.bt_neg;
@@ -475,7 +493,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 CU(mark(2));
                 CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
                 CU(mark(0));
-                CU(use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a7
+                CU(g.algorithm == 1 ? launch_alg1(p, ctas, st)
+                                    : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
                 CU(mark(0));
                 launches += 2;
                 ++g.st.step_launches;
@@ -493,6 +512,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaMemcpyAsync(&hs, g.dstats, sizeof hs, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     step_phase_report();
+    win_phase_report();
     if (window_set) {
         cudaStreamAttrValue a{};
         a.accessPolicyWindow.num_bytes = 0;
@@ -565,6 +585,16 @@ int w2v_debug_batches(uint8_t* keep, uint8_t* b, uint8_t* N, int32_t* ctx, int32
     if (N) CU(cudaMemcpyAsync(N, g.dbg_N, Lq, cudaMemcpyDefault, g.stream));
     if (ctx) CU(cudaMemcpyAsync(ctx, g.dbg_ctx, (size_t)Lq * 2 * g.window * 4, cudaMemcpyDefault, g.stream));
     if (neg) CU(cudaMemcpyAsync(neg, g.dbg_neg, (size_t)Lq * kk * 4, cudaMemcpyDefault, g.stream));
+    CU(cudaStreamSynchronize(g.stream));
+    return W2V_OK;
+}
+
+int w2v_debug_alg1_negatives(int32_t* neg) {
+    if (!g.live || g.dbg_rec_len == 0 || !g.dbg_a1neg)
+        return fail(W2V_ESTATE, "w2v_debug_alg1_negatives: nothing recorded (needs algorithm=1 and debug_len > 0)");
+    if (!neg) return fail(W2V_EINVAL, "w2v_debug_alg1_negatives: null out");
+    const int64_t kk = g.K > 0 ? g.K : 1;
+    CU(cudaMemcpyAsync(neg, g.dbg_a1neg, (size_t)g.dbg_rec_len * 2 * g.window * kk * 4, cudaMemcpyDefault, g.stream));
     CU(cudaStreamSynchronize(g.stream));
     return W2V_OK;
 }

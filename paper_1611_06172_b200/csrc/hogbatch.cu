@@ -362,7 +362,8 @@ void step_phase_report() {
 #if defined(W2V_PHASE_TIMING)
     unsigned long long h[8];
     cudaMemcpyFromSymbol(h, g_phase, sizeof h);
-    const double T = h[4] ? (double)h[4] : 1.0;
+    if (!h[4]) return;
+    const double T = (double)h[4];
     fprintf(stderr, "[phase] per target (cycles): chunk-load %.0f  gather->landed %.0f (issue+prep %.0f)  compute %.0f  scatter->done %.0f  targets %llu\n",
             h[0] / T, h[1] / T, h[5] / T, h[2] / T, h[3] / T, h[4]);
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -19,9 +19,20 @@
 //    (pass A, reads the snapshot) and ΔIn (pass B, writes value + accumulator rows).
 // Paper mapping: PAPER.md:116-126 (HogBatch GEMMs, write-back at the end), :140-149 (fewer
 // model updates), :135-138 (Hogwild across work units).
+#include <cstdio>
+
 #include "hogbatch_common.cuh"
 
 namespace w2v {
+
+#if defined(W2V_PHASE_TIMING)
+// (experiment) cycles per target summed over warps: waits for this target's rows, prefetch of
+// the next target (incl. conflict waits), compute, scatter issue; targets
+__device__ unsigned long long g_wphase[8];
+#define W2V_T(...) __VA_ARGS__
+#else
+#define W2V_T(...)
+#endif
 
 namespace {
 
@@ -78,6 +89,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
     uint32_t phA = 0, phB0 = 0, phB1 = 0;
     unsigned gstep = 0;
 
+    W2V_T(unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0, st_tail_pairs = 0;
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
@@ -177,6 +189,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         int64_t q_next = -1;
         float alpha = 0.f;
         for (int m = 0; m < nk; ++m, ++gstep) {
+            W2V_T(long long t0 = clock64();)
             const int cur = gstep & 1, nxt = cur ^ 1;
             float* Bc = Bb + cur * KP1MAX * RS;
             const float* Bp = Bb + nxt * KP1MAX * RS;
@@ -185,6 +198,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
             if (cur) phB1 ^= 1u; else phB0 ^= 1u;
             mbar_wait(mbarA, phA);
             phA ^= 1u;
+            W2V_T(long long t1 = clock64(); ph[0] += t1 - t0;)
             // exactness: rows of target m repeated from target m-1 get its ΔOut (still in Bp)
             if (m > 0) {
                 const int32_t* bidp = bid + nxt * KP1MAX;
@@ -250,6 +264,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
             }
             __syncwarp();
 
+            W2V_T(long long t2 = clock64(); ph[1] += t2 - t1;)
             // ---------------- a4/a5: all N x (K+1) dots, reduce-scatter, E, G, loss
             float2 bq[KP1MAX][CP2];
 #pragma unroll
@@ -347,6 +362,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
             fence_proxy_async_smem();
             __syncwarp();
 
+            W2V_T(long long t3 = clock64(); ph[2] += t3 - t2;)
             // ---------------- a7: ΔOut rows now; position m-w leaves the window
             if (lane < KP1)
                 bulk_red_add_s2g_hint(p.M + (size_t)bidc[lane] * 2 * D + D, Bc + lane * RS, rowbytes,
@@ -371,6 +387,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
                 for (int i = lane; i < N; i += 32) p.dbg_ctx[q * 2 * w + i] = kid[lo + i + (lo + i >= m ? 1 : 0)];
                 for (int k = lane; k < K; k += 32) p.dbg_neg[q * K + k] = bidc[1 + k];
             }
+            W2V_T(ph[3] += clock64() - t3; ph[4] += 1;)
             if (p.deterministic) __threadfence();
             __syncwarp();
         }
@@ -385,6 +402,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         st_loss += __shfl_xor_sync(kFull, st_loss, o);
         st_tail += __shfl_xor_sync(kFull, st_tail, o);
     }
+    W2V_T(if (lane == 0) for (int i = 0; i < 8; ++i) atomicAdd(&g_wphase[i], ph[i]);)
     if (lane == 0) {
         atomicAdd(&p.stats->words, st_words);
         atomicAdd(&p.stats->targets, st_targets);
@@ -425,6 +443,19 @@ const Inst* pick(int D, int K) {
 }
 
 }  // namespace
+
+void win_phase_report() {
+#if defined(W2V_PHASE_TIMING)
+    unsigned long long h[8];
+    cudaMemcpyFromSymbol(h, g_wphase, sizeof h);
+    if (!h[4]) return;
+    const double T = (double)h[4];
+    fprintf(stderr, "[phase] win per target (cycles): wait rows %.0f  prefetch next %.0f  compute %.0f  scatter issue %.0f  targets %llu\n",
+            h[0] / T, h[1] / T, h[2] / T, h[3] / T, h[4]);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_wphase, z, sizeof z);
+#endif
+}
 
 size_t win_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     const Inst* in = pick(D, K);

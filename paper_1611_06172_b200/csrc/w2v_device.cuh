@@ -6,7 +6,7 @@
 
 namespace w2v {
 
-enum : uint32_t { kTagPos = 1, kTagNeg = 2, kTagInit = 3 };
+enum : uint32_t { kTagPos = 1, kTagNeg = 2, kTagInit = 3, kTagA1Neg = 6 };
 
 // C1: Philox4x32-10, key = seed, counter = (p lo, p hi, e, tag<<24 | idx).
 struct U4 { uint32_t x, y, z, w; };

@@ -55,6 +55,8 @@ struct StepParams {
     // prefix) get evict_last if l2_hint & 1; the others evict_first if l2_hint & 2
     int64_t hot_rows;
     int32_t l2_hint;
+    int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)
+    int32_t* dbg_a1neg;   // Alg.1 debug: [len][2*window][K] per-input negatives
 };
 
 // setup.cu
@@ -72,6 +74,13 @@ cudaError_t launch_batch(const StepParams& p, int sms, cudaStream_t st);
 size_t win_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
 int win_max_ctas_per_sm(const StepParams& p);
 cudaError_t launch_win(const StepParams& p, int ctas, cudaStream_t st);
+void win_phase_report();  // (experiment builds with W2V_PHASE_TIMING)
+
+// alg1.cu (Algorithm 1, the level-1 baseline)
+bool alg1_supported(int D, int K);
+size_t alg1_warp_bytes(int L);
+int alg1_max_ctas_per_sm(const StepParams& p);
+cudaError_t launch_alg1(const StepParams& p, int ctas, cudaStream_t st);
 
 // hogbatch.cu (per-target rows; any window)
 bool step_supported(int D, int K);

@@ -195,7 +195,7 @@ def heldout_loss(M_in, M_out, cfg, n0, n):
     return st["loss_sum"] / st["loss_pairs"]
 
 
-def oracle_train_tail(ids, cfg, tail_from, prec="f32", debug=None):
+def oracle_train_tail(ids, cfg, tail_from, prec="f32", debug=None, algorithm=0):
     """oracle.train split at chunk-aligned position `tail_from` so the loss of the final part
     is reported separately (same arithmetic as one call: setup, then train_range in order)."""
     n = ids.size
@@ -204,7 +204,8 @@ def oracle_train_tail(ids, cfg, tail_from, prec="f32", debug=None):
     mi, mo = oracle.init(cfg.V, cfg.D, cfg.seed)
     dt = oracle.real_dtype(prec)
     M_in, M_out = mi.astype(dt), mo.astype(dt)
-    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, n)
+    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, n,
+                             algorithm=algorithm)
     dbg = oracle.Debug(debug[0], debug[1], cfg.window, cfg.K) if debug else None
     head, tail = oracle.OrcStats(), oracle.OrcStats()
     split = tail_from // cfg.L
