@@ -351,6 +351,37 @@ def test_update_count_hogbatch_vs_alg1():
     assert hb["row_touches"] < a1["row_touches"]
 
 
+def test_alg1_per_input_negatives():
+    """Alg.1 l.10 draws its negatives per input word (reading R4 contrasts HogBatch's shared set):
+    O-A1's recorded per-input negatives never equal the target, follow q/P[V] renormalised without
+    the target (chi-square over all inputs), differ between the inputs of one target (independent
+    draws), and the training step they feed is Alg.1 verbatim (loss pairs N(K+1))."""
+    from scipy import stats
+    V, window, K = 10, 3, 5
+    ids = inputs.Corpus("iid", V, 0.7, 5).tokens(0, 6_000)
+    _, _, st, dbg = oracle.train(ids, V, 4, window, K, 0.01, 0.0, 9, 200, algorithm=1, debug=(0, ids.size))
+    c = oracle.counts(ids, V)
+    q = np.diff(oracle.sampler(c)).astype(np.float64)
+    hist = np.zeros(V)
+    distinct_inputs = 0
+    for p in np.flatnonzero(dbg.N):
+        N = int(dbg.N[p])
+        negs = dbg.a1neg[p, :N, :]
+        assert np.all(negs >= 0) and np.all(negs != ids[p])
+        assert np.all(dbg.a1neg[p, N:, :] == -1)
+        distinct_inputs += int(len({tuple(r) for r in negs}) == N)
+        hist += np.bincount(negs.ravel(), minlength=V)
+    assert distinct_inputs > 0.95 * np.count_nonzero(dbg.N)
+    # pooled over targets the expected share of w is sum_t q_w / (P - q_t) (w != t)
+    exp = np.zeros(V)
+    for p in np.flatnonzero(dbg.N):
+        pexp = q.copy(); pexp[ids[p]] = 0; pexp /= pexp.sum()
+        exp += pexp * int(dbg.N[p]) * K
+    m = exp > 5
+    assert stats.chisquare(hist[m], exp[m] * hist[m].sum() / exp[m].sum()).pvalue > 1e-4
+    assert st["loss_pairs"] == int(dbg.N.astype(np.int64).sum() * (K + 1))
+
+
 # ---------------------------------------------------------------- init / alpha ---------------
 def test_init_range_and_distribution():
     """Reading R10: M_in ~ U[-0.5/D, 0.5/D), M_out = 0, deterministic."""
