@@ -163,6 +163,8 @@ def run_ours(args):
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", SYNC_P)
+    w2v.set_option("sync_hot_rows", args.sync_hot_rows)      # C14 (0 = C13 full averaging)
+    w2v.set_option("sync_cold_every", args.sync_cold_every)
     w2v.set_option("kernel", args.kernel)
     w2v.set_option("algorithm", 1 if args.algorithm == "alg1" else 0)
     stream = torch.cuda.current_stream()
@@ -230,6 +232,9 @@ def run_ours(args):
             "config": {"workload": "cfg3: V=1,000,000 D=300 window=5 K=5 t=1e-4 alpha=0.025, 800M planted "
                                    "Zipf(1.07) tokens (C=10,000, L=20), 1 epoch per step",
                        "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": SYNC_P if world > 1 else None,
+                       "sync": ("C13 full average" if args.sync_hot_rows == 0 else
+                                f"C14 hot rows [0,{args.sync_hot_rows}) every interval, rest every {args.sync_cold_every}")
+                       if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
                        "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "alg1"}.get(last["kernel"]),
@@ -267,6 +272,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 per-target rows, 2 window-resident rows")
     ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
+    ap.add_argument("--sync-hot-rows", type=int, default=0, help="C14 hot prefix averaged every interval (0 = all)")
+    ap.add_argument("--sync-cold-every", type=int, default=1, help="C14 cold rows averaged every this many intervals")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
                     help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")
     args = ap.parse_args()

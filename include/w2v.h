@@ -54,6 +54,7 @@ typedef struct {
                                 negatives; batch.cu), ms — not included in ms_step              */
     int64_t l2_window_bytes; /* a8: bytes of the hot-row prefix under the persisting-L2 window  */
     int64_t l2_carve_bytes;  /* a8: persisting-L2 carve-out set for the last w2v_train (0 = off) */
+    int64_t syncs_hot;       /* C14 averagings of the hot-row prefix only (syncs counts full ones) */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").
@@ -73,6 +74,10 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          (one work unit, targets in corpus order, R17)
  *  "sentence_len"          chunk length L of C5 (1..4096; default 1000)
  *  "sync_period_words"     P of C13 (>=1; default 2^20)
+ *  "sync_hot_rows"         C14: rows [0,H) of both matrices (the Zipf-hot prefix)
+ *                          are averaged after every interval (default 0 = all rows, i.e. C13)
+ *  "sync_cold_every"       C14: rows [H,V) only after every this many intervals and after the
+ *                          last interval of each epoch (>=1; default 1)
  *  "lr_quantum"            Q of C8 (>=1; default 10000)
  *  "allow_target_negative" 0/1 (R2; default 0)
  *  "debug_base","debug_len" record the batch stream (C5-C7) for global positions

@@ -30,10 +30,22 @@ def sync_intervals(n: int, L: int, W: int, r: int, P: int) -> list[tuple[int, in
     return [(lo + k * I, hi if k == J - 1 else lo + (k + 1) * I) for k in range(J)]
 
 
+def synced_rows(k: int, J: int, V: int, hot_rows: int = 0, cold_every: int = 1) -> list[tuple[int, int]]:
+    """C14 (hot/cold averaging): row ranges averaged after interval k of
+    J. Rows [0, H) (the Zipf-hot prefix: ids are frequency ranks) after every interval; rows
+    [H, V) after every `cold_every`-th interval and after the last one of the epoch. H = 0 (or
+    >= V) or cold_every = 1 is C13's full average after every interval."""
+    H = V if hot_rows <= 0 or hot_rows >= V else hot_rows
+    if H == V or cold_every <= 1 or (k + 1) % cold_every == 0 or k == J - 1:
+        return [(0, V)]
+    return [(0, H)]
+
+
 def train_replica(ids_global, V, D, window, K, alpha0, t, seed, L, W, r, P, average, epochs=1,
-                  prec="f64", counts_global=None, debug=None, lr_quantum=10_000):
+                  prec="f64", counts_global=None, debug=None, lr_quantum=10_000, hot_rows=0, cold_every=1):
     """Run replica r of W on its shard. `average(M_in, M_out)` must replace both matrices by the
-    mean over replicas (called after every interval when W > 1). Returns (M_in, M_out, stats, dbg).
+    mean over replicas (called after every interval when W > 1, with row-slice views of the
+    matrices when C14 averages only the hot prefix). Returns (M_in, M_out, stats, dbg).
     """
     from . import Debug
     n = ids_global.size
@@ -49,8 +61,10 @@ def train_replica(ids_global, V, D, window, K, alpha0, t, seed, L, W, r, P, aver
     dbg = Debug(debug[0], debug[1], window, K) if debug else None
     shard = np.ascontiguousarray(ids_global[start:end])
     for e in range(epochs):
-        for (a, b) in sync_intervals(n, L, W, r, P):
+        iv = sync_intervals(n, L, W, r, P)
+        for k, (a, b) in enumerate(iv):
             train_range(prm, thr, Ptab, shard, start, start, end - start, e, a, b, M_in, M_out, st, dbg, prec)
             if W > 1:
-                average(M_in, M_out)
+                for lo_r, hi_r in synced_rows(k, len(iv), V, hot_rows, cold_every):
+                    average(M_in[lo_r:hi_r], M_out[lo_r:hi_r])
     return M_in, M_out, st.as_dict(), dbg

@@ -80,6 +80,8 @@ struct Ctx {
     int mode = 0;
     int32_t L = 1000;
     int64_t sync_period = 1 << 20;
+    int64_t sync_hot_rows = 0;   // C14: hot prefix averaged every interval (0 = all rows)
+    int64_t sync_cold_every = 1; // C14: the other rows every this many intervals (and the last)
     int64_t Q = 10000;
     int allow_tn = 0;
     int64_t dbg_base = 0, dbg_len = 0;
@@ -202,10 +204,16 @@ Plan make_plan(int64_t n, int32_t L, int32_t W, int32_t r, int64_t P) {
 // GPU; averaging over one replica is the identity).
 bool dp() { return g.comm != nullptr; }
 
-int sync_models() {
+// a9: replace rows [row_lo, row_hi) of both matrices (one contiguous range of the interleaved
+// model) by their mean over ranks
+int sync_models(int64_t row_lo = 0, int64_t row_hi = -1) {
     if (!dp()) return W2V_OK;
-    NC(g_nccl.allReduce(g.M, g.M, (size_t)g.V * 2 * g.D, ncclFloat32, ncclAvg, g.comm, g.stream));
-    g.st.syncs += 1;
+    if (row_hi < 0) row_hi = g.V;
+    if (row_hi <= row_lo) return W2V_OK;
+    NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.D, g.M + (size_t)row_lo * 2 * g.D,
+                        (size_t)(row_hi - row_lo) * 2 * g.D, ncclFloat32, ncclAvg, g.comm, g.stream));
+    if (row_lo == 0 && row_hi == g.V) g.st.syncs += 1;
+    else g.st.syncs_hot += 1;
     return W2V_OK;
 }
 
@@ -258,6 +266,8 @@ int w2v_set_option(const char* key, int64_t v) {
     if (k == "mode") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "mode must be 0 or 1"); g.mode = (int)v; }
     else if (k == "sentence_len") { if (v < 1 || v > 4096) return fail(W2V_EINVAL, "sentence_len out of [1,4096]"); g.L = (int32_t)v; }
     else if (k == "sync_period_words") { if (v < 1) return fail(W2V_EINVAL, "sync_period_words must be >= 1"); g.sync_period = v; }
+    else if (k == "sync_hot_rows") { if (v < 0) return fail(W2V_EINVAL, "sync_hot_rows must be >= 0"); g.sync_hot_rows = v; }
+    else if (k == "sync_cold_every") { if (v < 1) return fail(W2V_EINVAL, "sync_cold_every must be >= 1"); g.sync_cold_every = v; }
     else if (k == "lr_quantum") { if (v < 1) return fail(W2V_EINVAL, "lr_quantum must be >= 1"); g.Q = v; }
     else if (k == "allow_target_negative") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "allow_target_negative must be 0/1"); g.allow_tn = (int)v; }
     else if (k == "debug_base") { if (v < 0) return fail(W2V_EINVAL, "debug_base must be >= 0"); g.dbg_base = v; }
@@ -499,9 +509,11 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 launches += 2;
                 ++g.st.step_launches;
             }
-            if (dp()) {
+            if (dp()) {  // C13 / C14: full average, or the hot prefix with the cold rows every C-th
                 CU(mark(1));
-                int rc = sync_models();
+                const int64_t H = (g.sync_hot_rows <= 0 || g.sync_hot_rows >= g.V) ? g.V : g.sync_hot_rows;
+                const bool full = H == g.V || g.sync_cold_every <= 1 || (k + 1) % g.sync_cold_every == 0 || k == J - 1;
+                int rc = full ? sync_models() : sync_models(0, H);
                 if (rc) return rc;
                 CU(mark(1));
             }

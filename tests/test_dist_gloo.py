@@ -31,7 +31,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, hot_rows=0, cold_every=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -46,7 +46,7 @@ def _worker(rank, world, port, outdir):
 
     def average(M_in, M_out):
         for M in (M_in, M_out):
-            t = torch.from_numpy(M)
+            t = torch.from_numpy(M)   # a row-slice view when C14 averages only the hot prefix
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             t /= world
             g = [torch.empty_like(t) for _ in range(world)]
@@ -55,7 +55,8 @@ def _worker(rank, world, port, outdir):
         nsync[0] += 1
 
     M_in, M_out, st, dbg = odist.train_replica(ids, V, D, WINDOW, K, 0.025, T_SUB, SEED, L, world, rank, P,
-                                                average, counts_global=c_local.numpy(), debug=(start, end - start))
+                                                average, counts_global=c_local.numpy(), debug=(start, end - start),
+                                                hot_rows=hot_rows, cold_every=cold_every)
     plan = None
     try:
         from paper_1611_06172_b200 import binding
@@ -69,10 +70,13 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_two_replicas_gloo(tmp_path):
+@pytest.mark.parametrize("hot_rows,cold_every", [(0, 1), (60, 3)])
+def test_two_replicas_gloo(tmp_path, hot_rows, cold_every):
+    """C13 (full average after every interval) and C14 (hot prefix every interval, cold rows
+    every 3rd and the last): union of streams == 1 replica, replicas identical at the end."""
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), hot_rows, cold_every), nprocs=world,
+                       join=True, start_method="spawn")
     r = [np.load(os.path.join(tmp_path, f"r{k}.npz")) for k in range(world)]
     ids = inputs.Corpus("iid", V, 1.0, SEED).tokens(0, N_TOK, threads=1)
     _, _, st1, dbg1 = oracle.train(ids, V, D, WINDOW, K, 0.025, T_SUB, SEED, L, debug=(0, N_TOK))
@@ -82,7 +86,10 @@ def test_two_replicas_gloo(tmp_path):
     assert sum(int(x["words"]) for x in r) == st1["words"] == N_TOK
     # replicas identical after the final sync, and sync counts identical
     assert np.array_equal(r[0]["M_in"], r[1]["M_in"]) and np.array_equal(r[0]["M_out"], r[1]["M_out"])
-    assert int(r[0]["nsync"]) == int(r[1]["nsync"]) == len(odist.sync_intervals(N_TOK, L, world, 0, P))
+    J = len(odist.sync_intervals(N_TOK, L, world, 0, P))
+    assert int(r[0]["nsync"]) == int(r[1]["nsync"]) == J
+    full = sum(odist.synced_rows(k, J, V, hot_rows, cold_every) == [(0, V)] for k in range(J))
+    assert full == (J if hot_rows == 0 else len([k for k in range(J) if (k + 1) % cold_every == 0 or k == J - 1]))
     assert float(r[0]["disc"]) == 0.0
     # the library's host planner (if built) matches the protocol on both ranks
     for k in range(world):
@@ -111,3 +118,41 @@ def test_shard_plan_partitions():
         assert all(got[i][1] == got[i + 1][0] for i in range(W - 1))
         J = {len(odist.sync_intervals(n, L_, W, r, 4096)) for r in range(W)}
         assert len(J) == 1
+
+
+def _loss_worker(rank, world, port, outdir, hot_rows, cold_every):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    Vg, n = 2000, 240_000
+    ids = inputs.Corpus("iid", Vg, 1.0, 5).tokens(0, n, threads=1)
+    c = oracle.counts(ids, Vg)
+
+    def average(M_in, M_out):
+        for M in (M_in, M_out):
+            t = torch.from_numpy(M)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            t /= world
+
+    M_in, M_out, st, _ = odist.train_replica(ids, Vg, 32, 5, 5, 0.025, 1e-3, 11, 20, world, rank, 1 << 12,
+                                             average, counts_global=c, hot_rows=hot_rows, cold_every=cold_every)
+    if rank == 0:
+        held = inputs.Corpus("iid", Vg, 1.0, 5).tokens(n, 60_000, threads=1)
+        _, _, hs, _ = oracle.train(held, Vg, 32, 5, 5, 0.0, 1e-3, 12, 20, model=(M_in, M_out))
+        np.save(os.path.join(outdir, f"loss_{hot_rows}_{cold_every}.npy"), hs["loss_sum"] / hs["loss_pairs"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_hot_cold_averaging_loss_gate(tmp_path):
+    """C14 changes the sync semantics (SURVEY.md §8(f) NEXT-2 "gate it on loss"): 4 oracle replicas
+    with the hot 10% of rows averaged every interval and the cold rows every 4th interval reach a
+    held-out SGNS loss within 1% of C13's full averaging."""
+    world = 4
+    out = {}
+    for hot, every in ((0, 1), (200, 4)):
+        mp.start_processes(_loss_worker, args=(world, _free_port(), str(tmp_path), hot, every), nprocs=world,
+                           join=True, start_method="spawn")
+        out[(hot, every)] = float(np.load(os.path.join(tmp_path, f"loss_{hot}_{every}.npy")))
+    print(f"held-out loss/pair, 4 replicas: full average {out[(0, 1)]:.6f}, hot/cold {out[(200, 4)]:.6f}")
+    assert abs(out[(200, 4)] / out[(0, 1)] - 1) < 0.01

@@ -288,10 +288,12 @@ def test_cfg3_full_size_sampled_stream(w2v):
 
 
 # ------------------------------------------------------------------ data-parallel path --------
-def test_nccl_one_rank_dp_path_equals_plain(w2v):
+@pytest.mark.parametrize("hot_rows,cold_every", [(0, 1), (100, 3)])
+def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every):
     """The DP code path (C13: n_local all-gather, histogram all-reduce, sync intervals, model
-    averaging via NCCL) on a 1-rank communicator must reproduce the plain run exactly
-    (deterministic mode; mean of one replica = identity), with the expected sync count."""
+    averaging via NCCL; C14: hot-prefix averaging with the cold rows every 3rd interval) on a
+    1-rank communicator must reproduce the plain run exactly (deterministic mode; mean of one
+    replica = identity), with the expected full and hot-only sync counts."""
     cfg = inputs.CONFIGS[1]
     ids = cfg.corpus().tokens(0, cfg.n)
     plain = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
@@ -300,13 +302,18 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v):
     w2v.set_option("mode", 1)
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", 3000)
+    w2v.set_option("sync_hot_rows", hot_rows)
+    w2v.set_option("sync_cold_every", cold_every)
     w2v.dist_init(0, 1, w2v.dist_unique_id())
     w2v.train(torch.from_numpy(ids).cuda(), ids.size, 1)
     M_in = np.empty((cfg.V, cfg.D), np.float32); M_out = np.empty_like(M_in)
     w2v.get_embeddings(0, M_in); w2v.get_embeddings(1, M_out)
     st = w2v.get_stats()
     from oracle import dist as odist
-    assert st["syncs"] == len(odist.sync_intervals(cfg.n, cfg.L, 1, 0, 3000))
+    J = len(odist.sync_intervals(cfg.n, cfg.L, 1, 0, 3000))
+    full = sum(odist.synced_rows(k, J, cfg.V, hot_rows, cold_every) == [(0, cfg.V)] for k in range(J))
+    assert st["syncs"] == full and st["syncs_hot"] == J - full
+    assert (full < J) == (hot_rows > 0)
     assert np.array_equal(M_in, plain["M_in"]) and np.array_equal(M_out, plain["M_out"])
     w2v.sync()
     w2v.get_embeddings(0, M_in)
