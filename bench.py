@@ -237,7 +237,7 @@ def run_ours(args):
                        if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
-                       "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "alg1"}.get(last["kernel"]),
+                       "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1"}.get(last["kernel"]),
                        "algorithm": "hogbatch" if args.algorithm == "hogbatch" else "alg1 (PAPER.md:37-63, level-1 baseline)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic if args.algorithm == "hogbatch" else None,
@@ -270,7 +270,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 per-target rows, 2 window-resident rows")
+    ap.add_argument("--kernel", type=int, default=0,
+                    help="0 auto, 1 per-target rows, 2 window-resident rows, 3 window-resident warp-specialised")
     ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
     ap.add_argument("--sync-hot-rows", type=int, default=0, help="C14 hot prefix averaged every interval (0 = all)")
     ap.add_argument("--sync-cold-every", type=int, default=1, help="C14 cold rows averaged every this many intervals")

@@ -49,7 +49,8 @@ typedef struct {
     int64_t bytes_row;    /* algorithmic row bytes of the last w2v_train: row_touches*4D*2      */
     double  loss_tail_sum;   /* loss of targets at global positions >= option loss_tail_from    */
     int64_t loss_tail_pairs; /* ... and their pair count (the "final-10%" training loss)         */
-    int64_t kernel;          /* fused-step kernel of the last w2v_train: 1 rows, 2 window        */
+    int64_t kernel;          /* step kernel of the last w2v_train: 1 rows, 2 window, 3 window
+                                warp-specialised, 4 Alg.1                                       */
     double  ms_batch;        /* ... of which the a1/a2 batch kernel (subsampling, windows,
                                 negatives; batch.cu), ms — not included in ms_step              */
     int64_t l2_window_bytes; /* a8: bytes of the hot-row prefix under the persisting-L2 window  */
@@ -97,9 +98,9 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "ctas_per_sm"           0 = occupancy maximum (default), else that many 1-warp CTAs per SM
  *  "launch_words"          raw words per hogbatch_step launch (>=1; default 2^26): bounds a
  *                          launch's duration; results do not depend on it in deterministic mode
- *  "kernel"                0 auto (default; currently = 1, the faster on B200 for the paper's
- *                          shapes), 1 per-target rows (hogbatch.cu), 2 window-
- *                          resident rows (hogbatch_win.cu; window <= 15)
+ *  "kernel"                0 auto (default), 1 per-target rows (hogbatch.cu),
+ *                          2 window-resident rows (hogbatch_win.cu; window <= 15), 3 window-
+ *                          resident warp-specialised (hogbatch_wg.cu; window <= 15)
  *  "loss_tail_from"        global position from which targets also accumulate into
  *                          loss_tail_sum / loss_tail_pairs (default: never)
  *  "epochs_total"          E used by the alpha schedule when training is split over several

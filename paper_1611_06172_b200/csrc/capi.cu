@@ -281,7 +281,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
-    else if (k == "kernel") { if (v < 0 || v > 2) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows) or 2 (window)"); g.kernel = (int)v; }
+    else if (k == "kernel") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window) or 3 (window, warp-specialised)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
     else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
@@ -438,29 +438,34 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.algorithm = g.algorithm;
     if (g.algorithm == 1 && !alg1_supported(g.D, g.K))
         return fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K);
-    // kernel choice: window-resident rows when the window fits, else per-target
-    int32_t off_win = 0, off_row = 0;
+    // kernel choice: 1 per-target rows, 2 window-resident (one warp per unit),
+    // 3 window-resident warp-specialised (a CTA of column warps + an IO warp per unit)
+    int32_t off_win = 0, off_row = 0, off_wg = 0;
     const size_t wb_win = win_warp_bytes(g.L, g.window, g.K, g.D, &off_win);
     const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row);
+    const size_t wb_wg = wg_cta_bytes(g.L, g.window, g.K, g.D, &off_wg);
     const size_t kSmemMax = 227 * 1024;
-    bool use_win = wb_win > 0 && wb_win <= kSmemMax;
-    if (g.kernel != 2) use_win = false;  // auto = per-target rows (measured faster)
-    if (g.kernel == 2 && !use_win)
+    int kern = g.kernel == 0 ? 1 : g.kernel;
+    if (g.algorithm == 1) kern = 0;  // alg1.cu
+    if (kern == 2 && !(wb_win > 0 && wb_win <= kSmemMax))
         return fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
-    if (g.algorithm == 1) use_win = false;
-    size_t wb = use_win ? wb_win : wb_row;
-    if (g.algorithm == 1) wb = alg1_warp_bytes(g.L);
-    p.slab_offset = use_win ? off_win : off_row;
-    if (wb == 0 || wb > kSmemMax) return fail(W2V_EINVAL, "w2v_train: per-warp shared memory %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
+    if (kern == 3 && !(wb_wg > 0 && wb_wg <= kSmemMax))
+        return fail(W2V_EINVAL, "w2v_train: kernel=3 (window, warp-specialised) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
+    const bool use_win = kern == 2;
+    size_t wb = kern == 3 ? wb_wg : use_win ? wb_win : wb_row;
+    if (kern == 0) wb = alg1_warp_bytes(g.L);
+    p.slab_offset = kern == 3 ? off_wg : use_win ? off_win : off_row;
+    if (wb == 0 || wb > kSmemMax) return fail(W2V_EINVAL, "w2v_train: shared memory per work unit %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
     p.warp_bytes = (int32_t)wb;
     int ctas = 1;
     if (g.mode == 0) {
-        int occ = g.algorithm == 1 ? alg1_max_ctas_per_sm(p) : use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
-        if (occ < 1) return fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per warp)", wb);
+        int occ = kern == 0 ? alg1_max_ctas_per_sm(p) : kern == 3 ? wg_max_ctas_per_sm(p)
+                : use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
+        if (occ < 1) return fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per work unit)", wb);
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
-    g.st.kernel = g.algorithm == 1 ? 3 : use_win ? 2 : 1;
+    g.st.kernel = kern == 0 ? 4 : kern;  // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1
     CU(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
@@ -503,7 +508,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 CU(mark(2));
                 CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
                 CU(mark(0));
-                CU(g.algorithm == 1 ? launch_alg1(p, ctas, st)
+                CU(kern == 0 ? launch_alg1(p, ctas, st) : kern == 3 ? launch_wg(p, ctas, st)
                                     : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
                 CU(mark(0));
                 launches += 2;
@@ -525,6 +530,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaStreamSynchronize(st));
     step_phase_report();
     win_phase_report();
+    wg_phase_report();
     if (window_set) {
         cudaStreamAttrValue a{};
         a.accessPolicyWindow.num_bytes = 0;

@@ -76,6 +76,13 @@ int win_max_ctas_per_sm(const StepParams& p);
 cudaError_t launch_win(const StepParams& p, int ctas, cudaStream_t st);
 void win_phase_report();  // (experiment builds with W2V_PHASE_TIMING)
 
+// hogbatch_wg.cu (window-resident, warp-specialised: NW column warps + 1 IO warp per CTA)
+size_t wg_cta_bytes(int L, int window, int K, int D, int32_t* slab_offset);
+int wg_threads(int D);
+int wg_max_ctas_per_sm(const StepParams& p);
+cudaError_t launch_wg(const StepParams& p, int ctas, cudaStream_t st);
+void wg_phase_report();  // (experiment builds with W2V_PHASE_TIMING)
+
 // alg1.cu (Algorithm 1, the level-1 baseline)
 bool alg1_supported(int D, int K);
 size_t alg1_warp_bytes(int L);

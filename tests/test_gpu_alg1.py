@@ -28,7 +28,7 @@ def test_cfg1_alg1_deterministic(w2v, n):
     g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, n),
                 opts={"algorithm": 1})
     gneg = a1negs(w2v, n, cfg.window, cfg.K)
-    assert g["stats"]["kernel"] == 3
+    assert g["stats"]["kernel"] == 4
     o_in, o_out, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed,
                                             cfg.L, algorithm=1, debug=(0, n))
     for f in ("keep", "b", "N", "ctx"):

@@ -79,7 +79,8 @@ def test_init_bitexact(w2v):
 
 
 # ------------------------------------------------------------------ cfg1 parity --------------
-KERNELS = [1, 2]   # 1 = per-target rows (hogbatch.cu), 2 = window-resident rows (hogbatch_win.cu)
+KERNELS = [1, 2, 3]  # 1 = per-target rows (hogbatch.cu), 2 = window-resident rows (hogbatch_win.cu),
+                     # 3 = window-resident, warp-specialised (hogbatch_wg.cu)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)

@@ -77,7 +77,8 @@ def one(so, tokens, opts, reps, vmod=0):
 
 def run(names, tokens, sweeps, reps, vmod=0):
     for n in names:
-        so = os.path.join(OUT, f"libw2v_{n}.so")
+        so = os.path.join(OUT, f"libw2v_{n}.so") if n != "main" else \
+            os.path.join(ROOT, "paper_1611_06172_b200", "libw2v.so")
         for opts in sweeps:
             code = (f"import sys, json; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.dirname(__file__)!r});"
                     f"import ablate; print(json.dumps(ablate.one({so!r}, {tokens}, {opts!r}, {reps}, {vmod})))")
