@@ -30,6 +30,14 @@ import inputs  # noqa: E402
 
 METRIC = "words/sec (1/2/4/8 B200) and fraction of gather/scatter HBM roofline"
 CFG = 3
+WORKLOADS = {
+    3: "cfg3: V=1,000,000 D=300 window=5 K=5 t=1e-4 alpha=0.025, 800M planted Zipf(1.07) tokens "
+       "(C=10,000, L=20), 1 epoch per step",
+    4: "cfg4: V=1,000,000 D=128 window=8 K=15 t=1e-5 alpha=0.025, 800M iid Zipf(1.07) tokens (L=1000), "
+       "1 epoch per step",
+    5: "cfg5: V=4,000,000 D=300 window=5 K=5 t=1e-4 alpha=0.025, 8B iid Zipf(1.05) tokens generated "
+       "on-device (L=1000), 1 epoch per step",
+}
 SYNC_P = 1 << 20
 REF_SAMPLE = 1 << 17      # raw words per reference step (bounded CPU sample of cfg3)
 BASE_SAMPLE = 1 << 19     # raw words for the cpu_baseline leg
@@ -102,7 +110,8 @@ def cpu_baseline(cfg, sample):
     oracle.train_range(prm, thr, P, ids, 0, 0, sample, 0, 0, (sample + cfg.L - 1) // cfg.L, M_in, M_out, st)
     dt = time.perf_counter() - t0
     return {"value": sample / dt, "unit": "words/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {sample} raw words of cfg3 (V=1M, D=300), fp64 sequential O-HB, setup excluded",
+            "sample": f"first {sample} raw words of cfg{cfg.idx} (V={cfg.V}, D={cfg.D}), fp64 sequential O-HB, "
+                      "setup excluded",
             "seconds": dt}
 
 
@@ -151,18 +160,22 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = inputs.CONFIGS[CFG]
-    n = args.tokens if args.tokens else cfg.n      # --tokens: profiling only (prefix of cfg3)
+    cfg = inputs.CONFIGS[args.config]
+    n = args.tokens if args.tokens else cfg.n      # --tokens: profiling only (prefix of the config)
     start, end = w2v.dist_shard(n, cfg.L, world, rank)
     n_local = end - start
+    # the shard is generated on the device (inputs/gen_cuda.cu, bit-identical to the host
+    # generator; cfg5 is "generated on-device from seed") and copied once to pinned host memory
+    # for the e2e leg
+    dev = torch.empty(max(n_local, 1), dtype=torch.int32, device="cuda")
+    cfg.corpus().tokens_cuda(start, n_local, dev)
     host = torch.empty(max(n_local, 1), dtype=torch.int32, pin_memory=True)
-    cfg.corpus().tokens(start, n_local, out=host.numpy())
-    dev = host.cuda()
+    host.copy_(dev)
     torch.cuda.synchronize()
 
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
-    w2v.set_option("sync_period_words", SYNC_P)
+    w2v.set_option("sync_period_words", args.sync_period)
     w2v.set_option("sync_hot_rows", args.sync_hot_rows)      # C14 (0 = C13 full averaging)
     w2v.set_option("sync_cold_every", args.sync_cold_every)
     w2v.set_option("kernel", args.kernel)
@@ -223,24 +236,25 @@ def run_ours(args):
         achieved = last["bytes_row"] / (last["ms_step"] / 1e3) / 1e9   # GB/s, algorithmic bytes
         traffic = None   # DRAM bytes per launch (ncu --set full capture, profiles/), scaled to this launch size
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(prof):
-            traffic = json.load(open(prof)).get("dram_bytes_per_word") * n_local / max(last["step_launches"], 1)
+        if os.path.exists(prof) and args.algorithm == "hogbatch" and args.kernel in (0, 1):
+            tr = json.load(open(prof))
+            if tr.get("config", 3) == args.config:  # the capture is of this workload and kernel
+                traffic = tr.get("dram_bytes_per_word") * n_local / max(last["step_launches"], 1)
         out = {
             "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "cfg3: V=1,000,000 D=300 window=5 K=5 t=1e-4 alpha=0.025, 800M planted "
-                                   "Zipf(1.07) tokens (C=10,000, L=20), 1 epoch per step",
-                       "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": SYNC_P if world > 1 else None,
+            "config": {"workload": WORKLOADS[args.config],
+                       "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": args.sync_period if world > 1 else None,
                        "sync": ("C13 full average" if args.sync_hot_rows == 0 else
                                 f"C14 hot rows [0,{args.sync_hot_rows}) every interval, rest every {args.sync_cold_every}")
                        if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
-                       "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2",
+                       "l2": f"no flush: corpus ({n_local * 4 / 1e9:.1f} GB) and model ({cfg.V * cfg.D * 8 / 1e9:.2f} GB) exceed the 126 MB L2",
                        "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1"}.get(last["kernel"]),
                        "algorithm": "hogbatch" if args.algorithm == "hogbatch" else "alg1 (PAPER.md:37-63, level-1 baseline)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic if args.algorithm == "hogbatch" else None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "kernel": "hogbatch_step" if args.algorithm == "hogbatch" else "alg1",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
@@ -254,8 +268,11 @@ def run_ours(args):
                       "ms_setup": last["ms_setup"], "ms_step": last["ms_step"], "ms_sync": last["ms_sync"],
                       "syncs": last["syncs"]},
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and cfg.V * cfg.D <= 300_000_000:
             out["cpu_baseline"] = cpu_baseline(cfg, BASE_SAMPLE)
+        elif world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = {"value": None, "unit": "words/s", "cores": 1, "kind": "oracle",
+                                   "sample": "skipped: the fp64 oracle model (2*V*D*8 bytes) exceeds the host budget"}
         print(json.dumps(out))
     w2v.finalize()
     if world > 1:
@@ -273,6 +290,9 @@ def main():
     ap.add_argument("--kernel", type=int, default=0,
                     help="0 auto, 1 per-target rows, 2 window-resident rows, 3 window-resident warp-specialised")
     ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
+    ap.add_argument("--config", type=int, choices=[3, 4, 5], default=CFG,
+                    help="BASELINE.json config (3 = the headline workload; 4, 5 = the larger-tile / 4M-vocab ones)")
+    ap.add_argument("--sync-period", type=int, default=SYNC_P, help="words per GPU between model averagings")
     ap.add_argument("--sync-hot-rows", type=int, default=0, help="C14 hot prefix averaged every interval (0 = all)")
     ap.add_argument("--sync-cold-every", type=int, default=1, help="C14 cold rows averaged every this many intervals")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",

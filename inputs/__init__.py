@@ -25,7 +25,32 @@ def build(force: bool = False) -> str:
     return _SO
 
 
+_SRC_CUDA = os.path.join(_HERE, "gen_cuda.cu")
+_SO_CUDA = os.path.join(_HERE, "libw2v_inputs_cuda.so")
+
+
+def build_cuda(force: bool = False) -> str:
+    """The on-device copy of the generator (gen_cuda.cu), cross-compiled for sm_100a."""
+    if force or not os.path.exists(_SO_CUDA) or os.path.getmtime(_SO_CUDA) < os.path.getmtime(_SRC_CUDA):
+        nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+        subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
+                               "-shared", _SRC_CUDA, "-o", _SO_CUDA])
+    return _SO_CUDA
+
+
 _lib = None
+_lib_cuda = None
+
+
+def lib_cuda():
+    global _lib_cuda
+    if _lib_cuda is None:
+        _lib_cuda = ctypes.CDLL(build_cuda())
+        vp, i64, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64
+        _lib_cuda.gen_cuda_guide.argtypes = [vp, i64, ctypes.c_int, ctypes.c_int, vp, vp]
+        _lib_cuda.gen_cuda_iid.argtypes = [u64, vp, i64, vp, ctypes.c_int, i64, i64, vp, vp]
+        _lib_cuda.gen_cuda_planted.argtypes = [u64, i64, i64, i64, vp, vp, vp, i64, i64, vp, vp]
+    return _lib_cuda
 
 
 def lib():
@@ -92,6 +117,36 @@ class Corpus:
         else:
             lib().gen_planted(self.seed, self.V, self.C, self.Lg, _p(t[0], ctypes.c_uint64), _p(t[1], ctypes.c_uint64),
                               _p(t[2], ctypes.c_int64), i0, n, _p(out, ctypes.c_int32), th)
+        return out
+
+    def tokens_cuda(self, i0: int, n: int, out):
+        """Tokens i0 .. i0+n-1 generated on the GPU into the int32 CUDA tensor `out` (torch), on
+        torch's current stream; bit-identical to tokens() (integer-only kernel over the same
+        host-built u64 tables)."""
+        import torch
+        assert out.is_cuda and out.dtype == torch.int32 and out.is_contiguous() and out.numel() >= n
+        t = self._prep()
+        dev = out.device
+        st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        L = lib_cuda()
+        if self.kind == "iid":
+            pre = torch.from_numpy(t[0].view(np.int64)).to(dev)
+            Z = int(t[0][self.V])
+            bits = max(1, int(2 * self.V - 1).bit_length())
+            shift = max(0, Z.bit_length() - bits)
+            guide = torch.empty((1 << bits) + 1, dtype=torch.int32, device=dev)
+            rc = L.gen_cuda_guide(pre.data_ptr(), self.V, bits, shift, guide.data_ptr(), st)
+            rc = rc or L.gen_cuda_iid(self.seed, pre.data_ptr(), self.V, guide.data_ptr(), shift, i0, n,
+                                      out.data_ptr(), st)
+        else:
+            cl = torch.from_numpy(t[0].view(np.int64)).to(dev)
+            mem = torch.from_numpy(t[1].view(np.int64)).to(dev)
+            off = torch.from_numpy(t[2]).to(dev)
+            rc = L.gen_cuda_planted(self.seed, self.V, self.C, self.Lg, cl.data_ptr(), mem.data_ptr(), off.data_ptr(),
+                                    i0, n, out.data_ptr(), st)
+        torch.cuda.current_stream(dev).synchronize()
+        if rc != 0:
+            raise RuntimeError(f"gen_cuda launch failed: cudaError {rc}")
         return out
 
     def zipf_weights(self) -> np.ndarray:

@@ -1,5 +1,6 @@
 """Pins of the seeded input generator (inputs/): the recipe DESIGN.md §5 states."""
 import numpy as np
+import pytest
 from scipy import stats
 
 import inputs
@@ -52,3 +53,17 @@ def test_configs_match_baseline():
     assert (c[1].V, c[1].D, c[1].n, c[1].window, c[1].K, c[1].t) == (1000, 32, 20000, 2, 3, 0.0)
     assert (c[3].V, c[3].D, c[3].n, c[3].window, c[3].K, c[3].t) == (1_000_000, 300, 800_000_000, 5, 5, 1e-4)
     assert (c[4].V, c[4].D, c[4].window, c[4].K, c[4].t) == (1_000_000, 128, 8, 15, 1e-5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg_idx,i0,n", [(5, 0, 300_000), (5, 7_999_000_000, 200_000), (3, 123_456_789, 250_000),
+                                          (1, 0, 20_000), (4, 5_000_000, 100_000)])
+def test_gpu_generator_bitexact(cfg_idx, i0, n):
+    """The on-device generator (gen_cuda.cu; BASELINE cfg5 is generated on-device) reproduces the
+    host generator bit for bit on slices of the iid and planted corpora."""
+    import torch
+    cfg = inputs.CONFIGS[cfg_idx]
+    c = cfg.corpus()
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    c.tokens_cuda(i0, n, out)
+    assert np.array_equal(out.cpu().numpy(), c.tokens(i0, n))

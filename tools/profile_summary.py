@@ -59,7 +59,8 @@ def main(tag, csv_path, rep, bench_log):
     words = int(os.environ.get("W2V_PROFILED_WORDS", str(1 << 26)))
     traffic = {"dram_bytes_per_launch": dram_bytes, "words_per_launch": words,
                "dram_bytes_per_word": dram_bytes / words, "source": os.path.basename(rep), "round": tag,
-               "algorithmic_bytes_per_word": bench["roofline"]["row_bytes_per_word"]}
+               "algorithmic_bytes_per_word": bench["roofline"]["row_bytes_per_word"],
+               "config": int(os.environ.get("W2V_PROFILED_CONFIG", "3")), "kernel": "hogbatch_step (rows)"}
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     json.dump({k: {"value": v, "unit": u} for k, (v, u) in s.items()},
               open(os.path.join(ROOT, "profiles", f"{tag}_hogbatch_step_ncu.json"), "w"), indent=1)
