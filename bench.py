@@ -231,6 +231,19 @@ def run_ours(args):
     e2e_value = n * e2e_steps / (float(te[0]) / 1e3)
     last = steps[-1]
 
+    # row-path roof: the same kernel and batch stream with a4-a6 skipped (zero deltas reduced,
+    # model unchanged) — what the gathers + scatters alone sustain on this chip
+    roof = None
+    if args.algorithm == "hogbatch" and args.kernel in (0, 1):
+        w2v.set_option("rowpath_only", 1)
+        w2v.train(dev, n_local, 1)
+        rs = w2v.get_stats()
+        w2v.set_option("rowpath_only", 0)
+        tr = torch.tensor([rs["ms_step"]], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+        roof = n / (float(tr[0]) / 1e3)
+
     if rank == 0:
         peak, peak_src = peaks()
         achieved = last["bytes_row"] / (last["ms_step"] / 1e3) / 1e9   # GB/s, algorithmic bytes
@@ -260,6 +273,10 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
                          "row_bytes_per_word": last["bytes_row"] / n_local,
                          "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)},
+            "rowpath_roof": None if roof is None else {
+                "value": roof, "unit": "words/s", "frac": (n / (kern_max / 1e3)) / roof,
+                "how": "same step kernel, launch configuration and batch stream with a4-a6 skipped (zero "
+                       "deltas reduced): the gather/scatter path alone; frac = step-kernel words/s / roof"},
             "e2e": {"value": e2e_value, "unit": "words/s", "h2d_bytes_per_step": n_local * 4,
                     "d2h_bytes_per_step": 64},
             "gpu_launches": int(sum(s["launches"] for s in steps)),

@@ -101,6 +101,9 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "kernel"                0 auto (default), 1 per-target rows (hogbatch.cu),
  *                          2 window-resident rows (hogbatch_win.cu; window <= 15), 3 window-
  *                          resident warp-specialised (hogbatch_wg.cu; window <= 15)
+ *  "rowpath_only"          measurement mode (default 0): the rows kernel issues exactly the same
+ *                          gathers and scatters but skips a4-a6 and reduces zero deltas (model
+ *                          unchanged) — the achievable rate of the row path, for the roofline
  *  "loss_tail_from"        global position from which targets also accumulate into
  *                          loss_tail_sum / loss_tail_pairs (default: never)
  *  "epochs_total"          E used by the alpha schedule when training is split over several

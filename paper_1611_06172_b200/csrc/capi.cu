@@ -97,6 +97,7 @@ struct Ctx {
     int64_t loss_tail_from = INT64_MAX;
     int kernel = 0;  // 0 auto, 1 per-target rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
     int algorithm = 0;  // 0 HogBatch, 1 Alg.1 (alg1.cu)
+    int rowpath_only = 0;  // measurement mode of the rows kernel (StepParams::rowpath_only)
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -281,6 +282,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "ctas_per_sm") { if (v < 0 || v > 32) return fail(W2V_EINVAL, "ctas_per_sm out of [0,32]"); g.ctas_per_sm = (int)v; }
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
+    else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window) or 3 (window, warp-specialised)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
@@ -436,6 +438,9 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
     p.dbg_a1neg = g.dbg_a1neg;
     p.algorithm = g.algorithm;
+    p.rowpath_only = g.rowpath_only;
+    if (g.rowpath_only && (g.algorithm != 0 || (g.kernel != 0 && g.kernel != 1)))
+        return fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows kernel (kernel 0/1, algorithm 0)");
     if (g.algorithm == 1 && !alg1_supported(g.D, g.K))
         return fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K);
     // kernel choice: 1 per-target rows, 2 window-resident (one warp per unit),

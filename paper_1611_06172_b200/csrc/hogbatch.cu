@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             // butterfly reduce-scatter (lane l ends with dot l = t*KP1MAX + j), σ/G/loss once per
             // lane, G through smem; then per input: ΔOut += G·A (snapshot) and ΔIn over A.
 #ifndef W2V_ABL_NOCOMPUTE
+            if (p.rowpath_only) {
+                // measurement mode (option "rowpath_only"): the same gathers and scatters with
+                // a4-a6 skipped — zero deltas are reduced, the model is unchanged
+                float4* z = reinterpret_cast<float4*>(Bs);
+                for (int u = lane; u < (KP1MAX + 2 * window) * RS / 4; u += 32) z[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
             float2 bq[KP1MAX][CP2], dq[KP1MAX][CP2];
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
@@ -250,6 +256,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 #pragma unroll
                 for (int c = 0; c < CP2; ++c)
                     *reinterpret_cast<float2*>(Bs + j * RS + 2 * lane + 64 * c) = dq[j][c];
+            }
 #endif  // W2V_ABL_NOCOMPUTE
             fence_proxy_async_smem();
             __syncwarp();

@@ -55,6 +55,7 @@ struct StepParams {
     // prefix) get evict_last if l2_hint & 1; the others evict_first if l2_hint & 2
     int64_t hot_rows;
     int32_t l2_hint;
+    int32_t rowpath_only; // measurement mode: rows kernel without a4-a6 (zero deltas; model unchanged)
     int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)
     int32_t* dbg_a1neg;   // Alg.1 debug: [len][2*window][K] per-input negatives
 };

@@ -319,3 +319,29 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every):
     w2v.sync()
     w2v.get_embeddings(0, M_in)
     assert np.array_equal(M_in, plain["M_in"])
+
+
+def test_rowpath_only_measurement_mode(w2v):
+    """Option rowpath_only (the bench's row-path roof): the same batch stream and row traffic
+    (words, targets, row_touches identical), zero deltas — the model is bit-unchanged."""
+    cfg = inputs.CONFIGS[2]
+    ids = cfg.corpus().tokens(0, 400_000)
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("sentence_len", cfg.L)
+    M0 = np.empty((cfg.V, cfg.D), np.float32); w2v.get_embeddings(0, M0)
+    w2v.set_option("rowpath_only", 1)
+    dev = torch.from_numpy(ids).cuda()
+    w2v.train(dev, ids.size, 1)
+    a = w2v.get_stats()
+    M1 = np.empty_like(M0); w2v.get_embeddings(0, M1)
+    O1 = np.empty_like(M0); w2v.get_embeddings(1, O1)
+    assert np.array_equal(M0, M1) and not O1.any()
+    w2v.set_option("rowpath_only", 0)
+    w2v.train(dev, ids.size, 1)
+    b = w2v.get_stats()
+    for k in ("words", "targets", "row_touches"):
+        assert b[k] == 2 * a[k], k
+    w2v.set_option("kernel", 2)
+    w2v.set_option("rowpath_only", 1)
+    with pytest.raises(w2v.W2VError):
+        w2v.train(dev, ids.size, 1)
