@@ -11,8 +11,9 @@
  *    read/written during the call only and never retained. The library owns M_in, M_out,
  *    the sampler tables and all work buffers (cudaMalloc'd in w2v_init / w2v_train, freed in
  *    w2v_finalize).
- *  - Model layout in HBM (DESIGN.md §8): one buffer of V rows, row w = [M_in[w] | M_out[w]],
- *    2·D fp32 per row, so the Zipf-hot rows of BOTH matrices form one contiguous prefix.
+ *  - Model layout in HBM (DESIGN.md §7): one buffer of V rows, row w = [M_in[w] | M_out[w]],
+ *    each half padded to a multiple of 32 fp32 (128 B), so the Zipf-hot rows of BOTH matrices
+ *    form one contiguous prefix and every row starts on a cache line.
  *  - All work is enqueued on the library stream (w2v_set_stream, default: a private stream);
  *    every call returns after its work has completed (synchronous API).
  */

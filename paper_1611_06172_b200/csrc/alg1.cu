@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(32) alg1_kernel(const StepParams p) {
     int32_t* nk_s = reinterpret_cast<int32_t*>(wbase + 8);
     int32_t* kid = reinterpret_cast<int32_t*>(wbase + 16);
     int32_t* kinfo = kid + p.Lp;
-    const int D = p.D, K = p.K, W2 = 2 * p.window;
+    const int D = p.D, Ds = p.Ds, K = p.K, W2 = 2 * p.window;
     const int64_t shard_end = p.shard_start + p.n_local;
 
     // lane's columns: float2 c at d = 2*lane + 64c; the last float2 columns may be past D
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(32) alg1_kernel(const StepParams p) {
             }
             const int32_t* negm = p.bt_neg + (rel * p.Lp + m) * (int64_t)W2 * K;
             // l.8: the target row, in registers for the whole target (its updates go to both)
-            float* pt = p.M + (size_t)tw * 2 * D + D + 2 * lane;
+            float* pt = p.M + (size_t)tw * 2 * Ds + Ds + 2 * lane;
             float2 bt[CP2];
 #pragma unroll
             for (int c = 0; c < CP2; ++c) bt[c] = colok[c] ? ld_relaxed2(pt + 64 * c) : make_float2(0.f, 0.f);
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(32) alg1_kernel(const StepParams p) {
                 int32_t nid[KMAX];
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k) nid[k] = __shfl_sync(kFull, myneg, k < K ? k : 0);
-                float* pa = p.M + (size_t)in * 2 * D + 2 * lane;
+                float* pa = p.M + (size_t)in * 2 * Ds + 2 * lane;
                 float2 a[CP2], bn[KMAX][CP2];
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) a[c] = colok[c] ? ld_relaxed2(pa + 64 * c) : make_float2(0.f, 0.f);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(32) alg1_kernel(const StepParams p) {
                 for (int k = 0; k < KMAX; ++k)
 #pragma unroll
                     for (int c = 0; c < CP2; ++c)
-                        bn[k][c] = (k < K && colok[c]) ? ld_relaxed2(p.M + (size_t)nid[k] * 2 * D + D + 2 * lane + 64 * c)
+                        bn[k][c] = (k < K && colok[c]) ? ld_relaxed2(p.M + (size_t)nid[k] * 2 * Ds + Ds + 2 * lane + 64 * c)
                                                        : make_float2(0.f, 0.f);
                 // duplicates: a negative equal to the target, or to an earlier negative of
                 // this input, must read the value as updated by the earlier pairs (l.17)
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(32) alg1_kernel(const StepParams p) {
                     const float err = 0.0f - sg;
                     loss_t += (double)(fmaxf(inn, 0.f) - __logf(rc));
                     const float g = __fmul_rn(alpha, err);
-                    float* pn = p.M + (size_t)nid[k] * 2 * D + D + 2 * lane;
+                    float* pn = p.M + (size_t)nid[k] * 2 * Ds + Ds + 2 * lane;
 #pragma unroll
                     for (int c = 0; c < CP2; ++c) {
                         tmp[c] = ffma2(make_float2(err, err), bn[k][c], tmp[c]);

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -73,7 +74,7 @@ struct Ctx {
     bool live = false;
     int device = 0, sms = 148;
     int64_t V = 0;
-    int32_t D = 0, window = 0, K = 0;
+    int32_t D = 0, Ds = 0, window = 0, K = 0;  // Ds: half-row stride of the model (floats)
     float alpha = 0.f, t = 0.f;
     uint64_t seed = 0;
     // options
@@ -211,8 +212,8 @@ int sync_models(int64_t row_lo = 0, int64_t row_hi = -1) {
     if (!dp()) return W2V_OK;
     if (row_hi < 0) row_hi = g.V;
     if (row_hi <= row_lo) return W2V_OK;
-    NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.D, g.M + (size_t)row_lo * 2 * g.D,
-                        (size_t)(row_hi - row_lo) * 2 * g.D, ncclFloat32, ncclAvg, g.comm, g.stream));
+    NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.Ds, g.M + (size_t)row_lo * 2 * g.Ds,
+                        (size_t)(row_hi - row_lo) * 2 * g.Ds, ncclFloat32, ncclAvg, g.comm, g.stream));
     if (row_lo == 0 && row_hi == g.V) g.st.syncs += 1;
     else g.st.syncs_hot += 1;
     return W2V_OK;
@@ -237,11 +238,17 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
     g = fresh;
     CU(cudaGetDevice(&g.device));
     CU(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, g.device));
-    g.V = V; g.D = D; g.window = window; g.K = K; g.alpha = alpha; g.t = subsample; g.seed = seed;
+    g.V = V; g.D = D; g.window = window;
+    {   // model layout: each half-row padded to 128 B (W2V_ROW_ALIGN=0 packs them; experiment)
+        const char* ra = getenv("W2V_ROW_ALIGN");
+        const bool align = !(ra && ra[0] == '0');
+        g.Ds = align ? (D + 31) / 32 * 32 : D;
+    } g.K = K; g.alpha = alpha; g.t = subsample; g.seed = seed;
     CU(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     g.stream = g.own_stream;
     int rc;
-    if ((rc = dmalloc((void**)&g.M, (size_t)V * 2 * D * sizeof(float), "the model [M_in|M_out]"))) return rc;
+    if ((rc = dmalloc((void**)&g.M, (size_t)V * 2 * g.Ds * sizeof(float), "the model [M_in|M_out]"))) return rc;
+    CU(cudaMemsetAsync(g.M, 0, (size_t)V * 2 * g.Ds * sizeof(float), g.stream));  // padding stays 0
     if ((rc = dmalloc((void**)&g.counts, (size_t)V * 8, "counts"))) return rc;
     if ((rc = dmalloc((void**)&g.thr, (size_t)V * 8, "keep thresholds"))) return rc;
     if ((rc = dmalloc((void**)&g.P, (size_t)(V + 1) * 8, "sampler prefix"))) return rc;
@@ -254,7 +261,7 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
     if ((rc = dmalloc((void**)&g.info, sizeof(SetupInfo), "setup info"))) return rc;
     if ((rc = dmalloc((void**)&g.dstats, sizeof(DevStats), "stats"))) return rc;
     if ((rc = dmalloc((void**)&g.chunk_ctr, 64, "chunk counter"))) return rc;
-    CU(launch_init(g.M, V, D, seed, g.sms, g.stream));
+    CU(launch_init(g.M, V, D, g.Ds, seed, g.sms, g.stream));
     CU(cudaStreamSynchronize(g.stream));
     g.live = true;
     return W2V_OK;
@@ -397,7 +404,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g.device);
         cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g.device);
         if (maxp > 0 && maxwin > 0) {
-            const size_t rowb = (size_t)2 * g.D * 4;
+            const size_t rowb = (size_t)2 * g.Ds * 4;
             size_t carve = g.l2_carve_mb > 0 ? std::min<size_t>((size_t)g.l2_carve_mb << 20, (size_t)maxp) : (size_t)maxp;
             size_t bytes = g.l2_window_rows > 0 ? (size_t)g.l2_window_rows * rowb : carve;
             bytes = std::min<size_t>(bytes, (size_t)maxwin);
@@ -423,7 +430,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.shard_start = shard_start;
     p.n_local = n;
     p.n_global = n_global;
-    p.L = g.L; p.window = g.window; p.K = g.K; p.D = g.D;
+    p.L = g.L; p.window = g.window; p.K = g.K; p.D = g.D; p.Ds = g.Ds;
     p.epochs = g.epochs_total > 0 ? g.epochs_total : epochs;
     p.world = g.world;
     p.allow_tn = g.allow_tn;
@@ -433,7 +440,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.chunk_ctr = g.chunk_ctr; p.stats = g.dstats;
     p.loss_tail_from = g.loss_tail_from;
     p.l2_hint = g.l2_hint;
-    p.hot_rows = g.l2_hot_rows >= 0 ? g.l2_hot_rows : (int64_t)(64ll << 20) / ((int64_t)2 * g.D * 4);
+    p.hot_rows = g.l2_hot_rows >= 0 ? g.l2_hot_rows : (int64_t)(64ll << 20) / ((int64_t)2 * g.Ds * 4);
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
     p.dbg_a1neg = g.dbg_a1neg;
@@ -579,7 +586,7 @@ int w2v_get_embeddings(int32_t which, float* dst) {
     if (!g.live) return fail(W2V_ESTATE, "w2v_get_embeddings before w2v_init");
     if ((which != 0 && which != 1) || !dst) return fail(W2V_EINVAL, "w2v_get_embeddings: which must be 0/1, dst non-null");
     const size_t row = (size_t)g.D * 4;
-    CU(cudaMemcpy2DAsync(dst, row, g.M + (which ? g.D : 0), 2 * row, row, (size_t)g.V, cudaMemcpyDefault, g.stream));
+    CU(cudaMemcpy2DAsync(dst, row, g.M + (which ? g.Ds : 0), (size_t)2 * g.Ds * 4, row, (size_t)g.V, cudaMemcpyDefault, g.stream));
     CU(cudaStreamSynchronize(g.stream));
     return W2V_OK;
 }
@@ -588,7 +595,7 @@ int w2v_set_embeddings(int32_t which, const float* src) {
     if (!g.live) return fail(W2V_ESTATE, "w2v_set_embeddings before w2v_init");
     if ((which != 0 && which != 1) || !src) return fail(W2V_EINVAL, "w2v_set_embeddings: which must be 0/1, src non-null");
     const size_t row = (size_t)g.D * 4;
-    CU(cudaMemcpy2DAsync(g.M + (which ? g.D : 0), 2 * row, src, row, row, (size_t)g.V, cudaMemcpyDefault, g.stream));
+    CU(cudaMemcpy2DAsync(g.M + (which ? g.Ds : 0), (size_t)2 * g.Ds * 4, src, row, row, (size_t)g.V, cudaMemcpyDefault, g.stream));
     CU(cudaStreamSynchronize(g.stream));
     return W2V_OK;
 }

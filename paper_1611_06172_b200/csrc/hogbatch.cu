@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase);
     int32_t* nk_s = reinterpret_cast<int32_t*>(wbase + 8);   // kept count of the chunk
-    const int D = p.D, K = p.K, KP1 = K + 1, window = p.window, RMAX = 2 * window + KP1;
+    const int D = p.D, Ds = p.Ds, K = p.K, KP1 = K + 1, window = p.window, RMAX = 2 * window + KP1;
     const int KS = K > 0 ? K : 1;
     int32_t* kid = reinterpret_cast<int32_t*>(wbase + 16);   // kept ids of the chunk
     int32_t* kinfo = kid + p.Lp;                              // (offset << 8) | b
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 const int32_t id = rowid[r];
                 float* dst = r < N ? As + r * RS : Bs + (r - N) * RS;
 #ifndef W2V_ABL_NOGATHER
-                bulk_g2s_hint(dst, p.M + (size_t)id * 2 * D + (r < N ? 0 : D), rowbytes, mbar,
+                bulk_g2s_hint(dst, p.M + (size_t)id * 2 * Ds + (r < N ? 0 : Ds), rowbytes, mbar,
                               id < p.hot_rows ? pol_hot : pol_cold);
 #else
                 (void)dst; (void)id;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 if (id < W2V_ABL_NOHOT) continue;
 #endif
 #ifndef W2V_ABL_NOSCATTER
-                bulk_red_add_s2g_hint(p.M + (size_t)id * 2 * D + (r < N ? 0 : D), src, rowbytes,
+                bulk_red_add_s2g_hint(p.M + (size_t)id * 2 * Ds + (r < N ? 0 : Ds), src, rowbytes,
                                       id < p.hot_rows ? pol_hot : pol_cold);
 #else
                 (void)src; (void)id;

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), W2V_WG_MINB) hogbatch_wg_kernel
     constexpr int TI = 32 / KP1MAX;  // inputs per reduce-scatter tile
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool io = warp == NW;
-    const int D = p.D, K = p.K, KP1 = K + 1, w = p.window, S = 2 * w + 2, KS = K > 0 ? K : 1, RS = p.D;
+    const int D = p.D, Ds = p.Ds, K = p.K, KP1 = K + 1, w = p.window, S = 2 * w + 2, KS = K > 0 ? K : 1, RS = p.D;
     const int tiles = (2 * w + TI - 1) / TI;
     const uint32_t rowbytes = (uint32_t)D * 4u;
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), W2V_WG_MINB) hogbatch_wg_kernel
         if (lane == 0) mbar_arrive_expect_tx(mbarA + buf, bytesA);
         __syncwarp();
         if ((newslots >> lane) & 1u)
-            bulk_g2s_hint(val + lane * RS, p.M + (size_t)slot_id[lane] * 2 * D, rowbytes, mbarA + buf,
+            bulk_g2s_hint(val + lane * RS, p.M + (size_t)slot_id[lane] * 2 * Ds, rowbytes, mbarA + buf,
                           slot_id[lane] < p.hot_rows ? pol_hot : pol_cold);
         newslots = 0;
         bytesA = 0;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), W2V_WG_MINB) hogbatch_wg_kernel
         if (lane == 0) {
             slot_ref[s] = ref;
             if (ref == 0)
-                bulk_red_add_s2g_hint(p.M + (size_t)slot_id[s] * 2 * D, acc + s * RS, rowbytes,
+                bulk_red_add_s2g_hint(p.M + (size_t)slot_id[s] * 2 * Ds, acc + s * RS, rowbytes,
                                       slot_id[s] < p.hot_rows ? pol_hot : pol_cold);
         }
         if (ref == 0) {
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), W2V_WG_MINB) hogbatch_wg_kernel
         if (lane == 0) mbar_arrive_expect_tx(mbarB + buf, (uint32_t)KP1 * rowbytes);
         __syncwarp();
         if (lane < KP1)
-            bulk_g2s_hint(Bb + (buf * KP1MAX + lane) * RS, p.M + (size_t)ids[lane] * 2 * D + D, rowbytes,
+            bulk_g2s_hint(Bb + (buf * KP1MAX + lane) * RS, p.M + (size_t)ids[lane] * 2 * Ds + Ds, rowbytes,
                           mbarB + buf, ids[lane] < p.hot_rows ? pol_hot : pol_cold);
     };
 
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), W2V_WG_MINB) hogbatch_wg_kernel
                 W2V_T(long long t4 = clock64(); ph[3] += t4 - t3;)
                 if (lane < KP1) {
                     const int32_t id = bid[cur * KP1MAX + lane];
-                    bulk_red_add_s2g_hint(p.M + (size_t)id * 2 * D + D, Bb + (cur * KP1MAX + lane) * RS, rowbytes,
+                    bulk_red_add_s2g_hint(p.M + (size_t)id * 2 * Ds + Ds, Bb + (cur * KP1MAX + lane) * RS, rowbytes,
                                           id < p.hot_rows ? pol_hot : pol_cold);
                 }
                 if (m - w >= 0) leave(m - w);

@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
     constexpr int RS = 64 * CP2;
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;
-    const int D = p.D, K = p.K, KP1 = K + 1, w = p.window, S = 2 * w + 2, KS = K > 0 ? K : 1;
+    const int D = p.D, Ds = p.Ds, K = p.K, KP1 = K + 1, w = p.window, S = 2 * w + 2, KS = K > 0 ? K : 1;
     const uint32_t rowbytes = (uint32_t)D * 4u;
 
     uint64_t* mbarA = reinterpret_cast<uint64_t*>(wbase);  // window entries
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         if (lane == 0) mbar_arrive_expect_tx(mbarA, bytesA);
         __syncwarp();
         if ((newslots >> lane) & 1u)
-            bulk_g2s_hint(val + lane * RS, p.M + (size_t)slot_id[lane] * 2 * D, rowbytes, mbarA,
+            bulk_g2s_hint(val + lane * RS, p.M + (size_t)slot_id[lane] * 2 * Ds, rowbytes, mbarA,
                           slot_id[lane] < p.hot_rows ? pol_hot : pol_cold);
         newslots = 0;
         bytesA = 0;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         if (lane == 0) {
             slot_ref[s] = ref;
             if (ref == 0)
-                bulk_red_add_s2g_hint(p.M + (size_t)slot_id[s] * 2 * D, acc + s * RS, rowbytes,
+                bulk_red_add_s2g_hint(p.M + (size_t)slot_id[s] * 2 * Ds, acc + s * RS, rowbytes,
                                       slot_id[s] < p.hot_rows ? pol_hot : pol_cold);
         }
         if (ref == 0) {
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
         if (lane == 0) mbar_arrive_expect_tx(mbarB + buf, (uint32_t)KP1 * rowbytes);
         __syncwarp();
         if (lane < KP1)
-            bulk_g2s_hint(Bb + (buf * KP1MAX + lane) * RS, p.M + (size_t)ids[lane] * 2 * D + D, rowbytes, mbarB + buf,
+            bulk_g2s_hint(Bb + (buf * KP1MAX + lane) * RS, p.M + (size_t)ids[lane] * 2 * Ds + Ds, rowbytes, mbarB + buf,
                           ids[lane] < p.hot_rows ? pol_hot : pol_cold);
     };
 
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(32, W2V_WIN_MINB) hogbatch_win_kernel(const St
             W2V_T(long long t3 = clock64(); ph[2] += t3 - t2;)
             // ---------------- a7: ΔOut rows now; position m-w leaves the window
             if (lane < KP1)
-                bulk_red_add_s2g_hint(p.M + (size_t)bidc[lane] * 2 * D + D, Bc + lane * RS, rowbytes,
+                bulk_red_add_s2g_hint(p.M + (size_t)bidc[lane] * 2 * Ds + Ds, Bc + lane * RS, rowbytes,
                                       bidc[lane] < p.hot_rows ? pol_hot : pol_cold);
             if (m - w >= 0) leave(m - w);
             bulk_commit();

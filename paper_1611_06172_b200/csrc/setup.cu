@@ -141,7 +141,7 @@ __global__ void guide_kernel(const uint64_t* __restrict__ P, int64_t V, int32_t*
 
 // C9: M_in[r][d] = ((float)(u32>>8)*2^-24 - 0.5f) / (float)D, M_out = 0. D % 4 == 0, so the
 // 4 words of one Philox block land in one row.
-__global__ void init_kernel(float* __restrict__ M, int64_t V, int32_t D, uint64_t seed) {
+__global__ void init_kernel(float* __restrict__ M, int64_t V, int32_t D, int32_t Ds, uint64_t seed) {
     const int64_t groups = V * (int64_t)D / 4;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
         const U4 r = philox(seed, kTagInit, 0u, (uint64_t)g, 0u);
@@ -154,9 +154,9 @@ __global__ void init_kernel(float* __restrict__ M, int64_t V, int32_t D, uint64_
             const float f = __fmul_rn((float)(u[j] >> 8), 5.9604644775390625e-08f);
             vp[j] = __fdiv_rn(__fsub_rn(f, 0.5f), (float)D);
         }
-        float* rowp = M + row * 2 * (int64_t)D;
+        float* rowp = M + row * 2 * (int64_t)Ds;
         *reinterpret_cast<float4*>(rowp + d) = v;
-        *reinterpret_cast<float4*>(rowp + D + d) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(rowp + Ds + d) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -189,12 +189,12 @@ cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T
     return cudaGetLastError();
 }
 
-cudaError_t launch_init(float* M, int64_t V, int32_t D, uint64_t seed, int sms, cudaStream_t st) {
+cudaError_t launch_init(float* M, int64_t V, int32_t D, int32_t Ds, uint64_t seed, int sms, cudaStream_t st) {
     const int64_t groups = V * (int64_t)D / 4;
     int64_t blocks = (groups + 255) / 256;
     if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
     if (blocks < 1) blocks = 1;
-    init_kernel<<<(int)blocks, 256, 0, st>>>(M, V, D, seed);
+    init_kernel<<<(int)blocks, 256, 0, st>>>(M, V, D, Ds, seed);
     return cudaGetLastError();
 }
 

@@ -36,7 +36,8 @@ struct StepParams {
     const uint64_t* P;
     const int32_t* G;
     const SetupInfo* info;
-    float* M;  // interleaved model: row w = [M_in[w] (D) | M_out[w] (D)]
+    float* M;  // interleaved model: row w = [M_in[w] (D, padded to Ds) | M_out[w] (D, padded to Ds)]
+    int32_t Ds;  // half-row stride in floats (>= D)
     unsigned long long* chunk_ctr;
     DevStats* stats;
     int64_t loss_tail_from;
@@ -66,7 +67,7 @@ cudaError_t launch_hist(const int32_t* ids, int64_t n, int64_t V, unsigned long 
 cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T, float t, uint64_t* thr,
                           uint64_t* P, uint64_t* scratch, int32_t* G, int gbits, SetupInfo* info, cudaStream_t st,
                           int* launches);
-cudaError_t launch_init(float* M, int64_t V, int32_t D, uint64_t seed, int sms, cudaStream_t st);
+cudaError_t launch_init(float* M, int64_t V, int32_t D, int32_t Ds, uint64_t seed, int sms, cudaStream_t st);
 
 // batch.cu (a1 subsampling + window batching, a2 negative sampler)
 cudaError_t launch_batch(const StepParams& p, int sms, cudaStream_t st);
