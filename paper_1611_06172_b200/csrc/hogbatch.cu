@@ -193,6 +193,13 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 float v[32];
 #pragma unroll
                 for (int t = 0; t < TI; ++t) {
+#if !defined(W2V_DOT_FULL_TILE)
+                    if (i0 + t >= N) {  // warp-uniform: the last tile's missing inputs cost nothing
+#pragma unroll
+                        for (int j = 0; j < KP1MAX; ++j) v[t * KP1MAX + j] = 0.f;
+                        continue;
+                    }
+#endif
                     const float* Ai = As + (i0 + t < N ? i0 + t : 0) * RS + 2 * lane;
                     float2 a[CP2];
 #pragma unroll

@@ -32,6 +32,7 @@ VARIANTS = {
     "ldgsts_red_fence": ["-DW2V_GATHER_LDGSTS", "-DW2V_SCATTER_RED", "-DW2V_RED_FENCE"],
     "noscatter": ["-DW2V_ABL_NOSCATTER"],
     "phase": ["-DW2V_PHASE_TIMING"],
+    "fulltile": ["-DW2V_DOT_FULL_TILE"],
     "nohot16": ["-DW2V_ABL_NOHOT=16"],
     "nohot256": ["-DW2V_ABL_NOHOT=256"],
     "nohot4096": ["-DW2V_ABL_NOHOT=4096"],
