@@ -107,6 +107,32 @@ def test_cfg1_deterministic_parity(w2v, n, kernel):
     assert e_in <= 1e-5 and e_out <= 1e-5
 
 
+def test_cfg2_deterministic_parity_prefix(w2v):
+    """Deterministic mode at the paper's shape (BASELINE cfg2: V=71,000, D=300, window=5, K=5,
+    t=1e-4, planted Zipf(1.07)) on a 600,000-token prefix (~300K sequential targets, the rows
+    kernel in its conflict-serialised mode): bit-exact stream on a window, exact counters, and
+    both matrices within 1e-5 relative L2 of the fp64 oracle — the fp32 oracle's own distance to
+    fp64 is printed beside it (fp32 re-association over ~300K updates)."""
+    cfg = inputs.CONFIGS[2]
+    n = 600_000
+    ids = cfg.corpus().tokens(0, n)
+    dbgw = (n // 3, 3000)
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=dbgw)
+    o_in, o_out, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                            debug=dbgw)
+    assert_stream_equal(g["dbg"], o_dbg)
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert g["stats"][k] == o_st[k], k
+    f_in, f_out, _, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                     prec="f32")
+    e_in, e_out = rel_l2(g["M_in"], o_in), rel_l2(g["M_out"], o_out)
+    print(f"cfg2[:600K] deterministic: GPU vs fp64 oracle rel L2 M_in {e_in:.2e} M_out {e_out:.2e}; "
+          f"fp32 oracle vs fp64: {rel_l2(f_in, o_in):.2e} {rel_l2(f_out, o_out):.2e}; "
+          f"loss rel diff {abs(g['stats']['loss_sum'] / o_st['loss_sum'] - 1):.2e}")
+    assert e_in <= 1e-5 and e_out <= 1e-5
+    assert abs(g["stats"]["loss_sum"] / o_st["loss_sum"] - 1) <= 1e-5
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_cfg1_hogwild_stream_and_loss(w2v, kernel):
     """Hogwild mode (persistent grid, all SMs) on cfg1: the batch stream does not depend on the
