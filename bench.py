@@ -176,8 +176,12 @@ def run_ours(args):
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", args.sync_period)
-    w2v.set_option("sync_hot_rows", args.sync_hot_rows)      # C14 (0 = C13 full averaging)
-    w2v.set_option("sync_cold_every", args.sync_cold_every)
+    # C14 by default when N > 1: hot 10% of the rows averaged every interval, the rest every 16th
+    # (C14 and §10: C13's full 2.4 GB average per 2^20 words would dominate the step)
+    hot = args.sync_hot_rows if args.sync_hot_rows >= 0 else (cfg.V // 10 if world > 1 else 0)
+    cold = args.sync_cold_every if args.sync_cold_every > 0 else (16 if world > 1 else 1)
+    w2v.set_option("sync_hot_rows", hot)      # 0 = C13 full averaging
+    w2v.set_option("sync_cold_every", cold)
     w2v.set_option("kernel", args.kernel)
     w2v.set_option("algorithm", 1 if args.algorithm == "alg1" else 0)
     stream = torch.cuda.current_stream()
@@ -259,8 +263,8 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config],
                        "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": args.sync_period if world > 1 else None,
-                       "sync": ("C13 full average" if args.sync_hot_rows == 0 else
-                                f"C14 hot rows [0,{args.sync_hot_rows}) every interval, rest every {args.sync_cold_every}")
+                       "sync": ("C13 full average every interval" if hot == 0 else
+                                f"C14: rows [0,{hot}) averaged every interval, the rest every {cold}th and at the end")
                        if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": f"no flush: corpus ({n_local * 4 / 1e9:.1f} GB) and model ({cfg.V * cfg.D * 8 / 1e9:.2f} GB) exceed the 126 MB L2",
@@ -310,8 +314,10 @@ def main():
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=CFG,
                     help="BASELINE.json config (3 = the headline workload; 4, 5 = the larger-tile / 4M-vocab ones)")
     ap.add_argument("--sync-period", type=int, default=SYNC_P, help="words per GPU between model averagings")
-    ap.add_argument("--sync-hot-rows", type=int, default=0, help="C14 hot prefix averaged every interval (0 = all)")
-    ap.add_argument("--sync-cold-every", type=int, default=1, help="C14 cold rows averaged every this many intervals")
+    ap.add_argument("--sync-hot-rows", type=int, default=-1,
+                    help="C14 hot prefix averaged every interval (0 = all rows, C13; -1 = V/10 when N > 1)")
+    ap.add_argument("--sync-cold-every", type=int, default=0,
+                    help="C14 cold rows averaged every this many intervals (0 = 16 when N > 1)")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
                     help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")
     args = ap.parse_args()

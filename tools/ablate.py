@@ -46,13 +46,13 @@ def build(names):
         print(n, _build.build(out=os.path.join(OUT, f"libw2v_{n}.so"), extra=VARIANTS[n]), flush=True)
 
 
-def one(so, tokens, opts, reps, vmod=0):
+def one(so, tokens, opts, reps, vmod=0, config=3):
     import numpy as np  # noqa: F401
     import torch
     os.environ["W2V_LIBRARY"] = so
     import inputs
     from paper_1611_06172_b200 import binding as w2v
-    cfg = inputs.CONFIGS[3]
+    cfg = inputs.CONFIGS[config]
     host = torch.empty(tokens, dtype=torch.int32, pin_memory=True)
     cfg.corpus().tokens(0, tokens, out=host.numpy())
     V = cfg.V
@@ -76,13 +76,13 @@ def one(so, tokens, opts, reps, vmod=0):
             "l2_window_MB": best["l2_window_bytes"] / 2**20, "l2_carve_MB": best["l2_carve_bytes"] / 2**20}
 
 
-def run(names, tokens, sweeps, reps, vmod=0):
+def run(names, tokens, sweeps, reps, vmod=0, config=3):
     for n in names:
         so = os.path.join(OUT, f"libw2v_{n}.so") if n != "main" else \
             os.path.join(ROOT, "paper_1611_06172_b200", "libw2v.so")
         for opts in sweeps:
             code = (f"import sys, json; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.dirname(__file__)!r});"
-                    f"import ablate; print(json.dumps(ablate.one({so!r}, {tokens}, {opts!r}, {reps}, {vmod})))")
+                    f"import ablate; print(json.dumps(ablate.one({so!r}, {tokens}, {opts!r}, {reps}, {vmod}, {config})))")
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
             line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
             print(json.dumps({"variant": n, "opts": opts, "result": line}), flush=True)
@@ -98,6 +98,7 @@ if __name__ == "__main__":
     ap.add_argument("--tokens", type=int, default=1 << 27)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--occ", default="0", help="comma list of ctas_per_sm values (0 = max)")
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--vmod", type=int, default=0, help="experiment: ids %% vmod, V = vmod")
     ap.add_argument("--opts", default="", help="extra option sets: 'k=v,k=v;k=v' (each ';' part is one run)")
     a = ap.parse_args()
@@ -108,4 +109,4 @@ if __name__ == "__main__":
         sweeps = [{"ctas_per_sm": int(x)} if int(x) else {} for x in a.occ.split(",")]
         if a.opts:
             sweeps = [dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in part.split(",")) for part in a.opts.split(";")]
-        run(names, a.tokens, sweeps, a.reps, a.vmod)
+        run(names, a.tokens, sweeps, a.reps, a.vmod, a.config)
