@@ -102,6 +102,10 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "kernel"                0 auto (default), 1 per-target rows (hogbatch.cu),
  *                          2 window-resident rows (hogbatch_win.cu; window <= 15), 3 window-
  *                          resident warp-specialised (hogbatch_wg.cu; window <= 15)
+ *  "overlap_batch"         1: the a1/a2 batch kernel of launch j+1 runs on a side stream
+ *                          concurrently with the step kernel of launch j (double-buffered batch
+ *                          stream); 0 (default): serialised on the library stream — the
+ *                          co-resident batch block slows the step kernel by more than it hides
  *  "rowpath_only"          measurement mode (default 0): the rows kernel issues exactly the same
  *                          gathers and scatters but skips a4-a6 and reduces zero deltas (model
  *                          unchanged) — the achievable rate of the row path, for the roofline

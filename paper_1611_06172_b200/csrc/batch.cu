@@ -41,10 +41,13 @@ __device__ __forceinline__ int32_t neg_draw(const StepParams& p, uint32_t e, int
     return invcdf_guided(p.P, p.G, gshift, __umul64hi(u, PV));
 }
 
+// No shared memory (the redo masks live in a small global scratch): with ~1 KB of smem left by
+// the step kernel's slabs, one block of this kernel can co-reside on every SM and run the NEXT
+// launch range's batch stream while the step kernel consumes the current one (capi.cu).
 __global__ void __launch_bounds__(32 * kBatchWarps) batch_kernel(const StepParams p) {
-    __shared__ uint32_t redo[kBatchWarps][kMaskWords];  // targets whose first K draws hit a rejection
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t* fix = redo[wid];
+    // targets whose first K draws hit a rejection (one bit each), per warp
+    uint32_t* fix = p.bt_redo + ((size_t)blockIdx.x * kBatchWarps + wid) * kMaskWords;
     const uint32_t e = (uint32_t)p.epoch;
     const int window = p.window, K = p.K, KS = K > 0 ? K : 1, Lp = p.Lp;
     const int64_t shard_end = p.shard_start + p.n_local;
@@ -161,11 +164,14 @@ __global__ void __launch_bounds__(32 * kBatchWarps) batch_kernel(const StepParam
 
 }  // namespace
 
-cudaError_t launch_batch(const StepParams& p, int sms, cudaStream_t st) {
+size_t batch_redo_words(int sms) { return (size_t)sms * 8 * kBatchWarps * kMaskWords; }
+
+cudaError_t launch_batch(const StepParams& p, int sms, int blocks_per_sm, cudaStream_t st) {
     const int64_t chunks = p.chunk_hi - p.chunk_lo;
     if (chunks <= 0) return cudaSuccess;
     int64_t blocks = (chunks + kBatchWarps - 1) / kBatchWarps;
-    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+    if (blocks_per_sm < 1 || blocks_per_sm > 8) blocks_per_sm = 8;
+    if (blocks > (int64_t)sms * blocks_per_sm) blocks = (int64_t)sms * blocks_per_sm;
     batch_kernel<<<(int)blocks, 32 * kBatchWarps, 0, st>>>(p);
     return cudaGetLastError();
 }

@@ -113,8 +113,15 @@ struct Ctx {
     unsigned long long* chunk_ctr = nullptr;
     int64_t* dp_tmp = nullptr;
     // batch stream of one launch range (batch.cu -> step kernels), capacity in chunks
-    int32_t *bt_nk = nullptr, *bt_kid = nullptr, *bt_kinfo = nullptr, *bt_neg = nullptr;
-    size_t bt_cap_nk = 0, bt_cap_kid = 0, bt_cap_neg = 0;
+    // two sets: the batch kernel fills set (j+1)&1 on the side stream while the step kernel
+    // consumes set j&1 on the main stream
+    struct BtSet {
+        int32_t *nk = nullptr, *kid = nullptr, *kinfo = nullptr, *neg = nullptr;
+        size_t cap_nk = 0, cap_kid = 0, cap_neg = 0;
+    } bt[2];
+    uint32_t* bt_redo = nullptr;
+    cudaStream_t side = nullptr;
+    int overlap_batch = 0;  // option "overlap_batch" (measured slower on B200: DESIGN.md §8)
     // debug
     uint8_t *dbg_keep = nullptr, *dbg_b = nullptr, *dbg_N = nullptr;
     int32_t *dbg_ctx = nullptr, *dbg_neg = nullptr, *dbg_a1neg = nullptr;
@@ -128,9 +135,12 @@ struct Ctx {
 } g;
 
 void free_bt() {
-    cudaFree(g.bt_nk); cudaFree(g.bt_kid); cudaFree(g.bt_kinfo); cudaFree(g.bt_neg);
-    g.bt_nk = g.bt_kid = g.bt_kinfo = g.bt_neg = nullptr;
-    g.bt_cap_nk = g.bt_cap_kid = g.bt_cap_neg = 0;
+    for (auto& b : g.bt) {
+        cudaFree(b.nk); cudaFree(b.kid); cudaFree(b.kinfo); cudaFree(b.neg);
+        b = Ctx::BtSet{};
+    }
+    cudaFree(g.bt_redo);
+    g.bt_redo = nullptr;
 }
 
 void free_dbg() {
@@ -155,22 +165,25 @@ int dmalloc(void** p, size_t bytes, const char* what) {
 int ensure_bt(int64_t chunks, int32_t Lp, int32_t KS) {
     const size_t nk = (size_t)chunks, kid = (size_t)chunks * Lp, neg = (size_t)chunks * Lp * KS + 8 * (size_t)KS;
     int rc;
-    if (nk > g.bt_cap_nk) {
-        cudaFree(g.bt_nk); g.bt_nk = nullptr; g.bt_cap_nk = 0;
-        if ((rc = dmalloc((void**)&g.bt_nk, nk * 4, "batch stream (kept counts)"))) return rc;
-        g.bt_cap_nk = nk;
+    for (auto& b : g.bt) {
+        if (nk > b.cap_nk) {
+            cudaFree(b.nk); b.nk = nullptr; b.cap_nk = 0;
+            if ((rc = dmalloc((void**)&b.nk, nk * 4, "batch stream (kept counts)"))) return rc;
+            b.cap_nk = nk;
+        }
+        if (kid > b.cap_kid) {
+            cudaFree(b.kid); cudaFree(b.kinfo); b.kid = b.kinfo = nullptr; b.cap_kid = 0;
+            if ((rc = dmalloc((void**)&b.kid, kid * 4, "batch stream (kept words)"))) return rc;
+            if ((rc = dmalloc((void**)&b.kinfo, kid * 4, "batch stream (offsets, b)"))) return rc;
+            b.cap_kid = kid;
+        }
+        if (neg > b.cap_neg) {
+            cudaFree(b.neg); b.neg = nullptr; b.cap_neg = 0;
+            if ((rc = dmalloc((void**)&b.neg, neg * 4, "batch stream (negatives)"))) return rc;
+            b.cap_neg = neg;
+        }
     }
-    if (kid > g.bt_cap_kid) {
-        cudaFree(g.bt_kid); cudaFree(g.bt_kinfo); g.bt_kid = g.bt_kinfo = nullptr; g.bt_cap_kid = 0;
-        if ((rc = dmalloc((void**)&g.bt_kid, kid * 4, "batch stream (kept words)"))) return rc;
-        if ((rc = dmalloc((void**)&g.bt_kinfo, kid * 4, "batch stream (offsets, b)"))) return rc;
-        g.bt_cap_kid = kid;
-    }
-    if (neg > g.bt_cap_neg) {
-        cudaFree(g.bt_neg); g.bt_neg = nullptr; g.bt_cap_neg = 0;
-        if ((rc = dmalloc((void**)&g.bt_neg, neg * 4, "batch stream (negatives)"))) return rc;
-        g.bt_cap_neg = neg;
-    }
+    if (!g.bt_redo && (rc = dmalloc((void**)&g.bt_redo, batch_redo_words(g.sms) * 4, "batch kernel scratch"))) return rc;
     return W2V_OK;
 }
 
@@ -245,6 +258,7 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
         g.Ds = align ? (D + 31) / 32 * 32 : D;
     } g.K = K; g.alpha = alpha; g.t = subsample; g.seed = seed;
     CU(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking));
     g.stream = g.own_stream;
     int rc;
     if ((rc = dmalloc((void**)&g.M, (size_t)V * 2 * g.Ds * sizeof(float), "the model [M_in|M_out]"))) return rc;
@@ -290,6 +304,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
     else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
+    else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window) or 3 (window, warp-specialised)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
@@ -495,7 +510,26 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, negs_per_slot);
         if (rc) return rc;
     }
-    p.bt_nk = g.bt_nk; p.bt_kid = g.bt_kid; p.bt_kinfo = g.bt_kinfo; p.bt_neg = g.bt_neg;
+    p.bt_redo = g.bt_redo;
+    auto use_set = [&](StepParams& q, int set) {
+        q.bt_nk = g.bt[set].nk; q.bt_kid = g.bt[set].kid; q.bt_kinfo = g.bt[set].kinfo; q.bt_neg = g.bt[set].neg;
+    };
+    // the batch kernel of launch j+1 runs on the side stream while the step kernel of launch j
+    // runs on the main one (the step kernel's slabs leave room for one batch block per SM)
+    const bool ovl = g.overlap_batch != 0;
+    cudaEvent_t ev_tables, ev_bdone[2], ev_sdone[2];
+    CU(cudaEventCreateWithFlags(&ev_tables, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+        CU(cudaEventCreateWithFlags(&ev_bdone[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ev_sdone[i], cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(ev_tables, st));
+    if (ovl) {
+        CU(cudaStreamWaitEvent(g.side, ev_tables, 0));
+        for (int i = 0; i < 2; ++i) CU(cudaEventRecord(ev_sdone[i], st));
+    }
+    std::vector<cudaEvent_t> bev;  // (start, end) pairs of the batch launches on the side stream
+    int64_t jl = 0;                // launch counter (buffer set = jl & 1)
     std::vector<cudaEvent_t> evs;
     std::vector<int> ev_kind;  // 0 step, 1 sync, 2 batch
     auto mark = [&](int kind) -> cudaError_t {
@@ -512,17 +546,32 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         for (int64_t k = 0; k < J; ++k) {
             const int64_t ilo = dp() ? chunk_lo + k * pl.I : chunk_lo;
             const int64_t ihi = (dp() && k < J - 1) ? chunk_lo + (k + 1) * pl.I : chunk_hi;
-            for (int64_t a = ilo; a < ihi; a += per) {
+            for (int64_t a = ilo; a < ihi; a += per, ++jl) {
                 p.chunk_lo = a;
                 p.chunk_hi = std::min(ihi, a + per);
-                CU(mark(2));
-                CU(launch_batch(p, g.sms, st));  // a1 + a2 -> batch stream
-                CU(mark(2));
+                const int set = (int)(jl & 1);
+                use_set(p, set);
+                if (ovl) {  // a1 + a2 -> batch stream set `set`, once step jl-2 has consumed it
+                    CU(cudaStreamWaitEvent(g.side, ev_sdone[set], 0));
+                    cudaEvent_t b0, b1;
+                    CU(cudaEventCreate(&b0)); CU(cudaEventCreate(&b1));
+                    bev.push_back(b0); bev.push_back(b1);
+                    CU(cudaEventRecord(b0, g.side));
+                    CU(launch_batch(p, g.sms, 1, g.side));
+                    CU(cudaEventRecord(b1, g.side));
+                    CU(cudaEventRecord(ev_bdone[set], g.side));
+                    CU(cudaStreamWaitEvent(st, ev_bdone[set], 0));
+                } else {
+                    CU(mark(2));
+                    CU(launch_batch(p, g.sms, 8, st));
+                    CU(mark(2));
+                }
                 CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
                 CU(mark(0));
                 CU(kern == 0 ? launch_alg1(p, ctas, st) : kern == 3 ? launch_wg(p, ctas, st)
                                     : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
                 CU(mark(0));
+                if (ovl) CU(cudaEventRecord(ev_sdone[set], st));
                 launches += 2;
                 ++g.st.step_launches;
             }
@@ -560,6 +609,13 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         else if (ev_kind[i] == 1) g.st.ms_sync += ms;
         else g.st.ms_batch += ms;
     }
+    for (size_t i = 0; i + 1 < bev.size(); i += 2) {
+        CU(cudaEventElapsedTime(&ms, bev[i], bev[i + 1]));
+        g.st.ms_batch += ms;
+    }
+    for (auto e : bev) cudaEventDestroy(e);
+    cudaEventDestroy(ev_tables);
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(ev_bdone[i]); cudaEventDestroy(ev_sdone[i]); }
     for (auto e : evs) cudaEventDestroy(e);
     cudaEventDestroy(ev0); cudaEventDestroy(ev_h2d); cudaEventDestroy(ev_setup); cudaEventDestroy(ev_end);
     g.st.words += (int64_t)hs.words;
@@ -677,6 +733,8 @@ int w2v_finalize(void) {
     free_bt();
     cudaFree(g.M); cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
     cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
+    cudaStreamSynchronize(g.side);
+    cudaStreamDestroy(g.side);
     cudaStreamDestroy(g.own_stream);
     Ctx fresh;
     g = fresh;

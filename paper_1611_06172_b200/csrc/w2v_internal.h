@@ -52,6 +52,7 @@ struct StepParams {
     int32_t* bt_kid;      // [chunks][Lp]      kept words, corpus order
     int32_t* bt_kinfo;    // [chunks][Lp]      (offset << 8) | b
     int32_t* bt_neg;      // [chunks][Lp][KS]  shared negatives of each kept target
+    uint32_t* bt_redo;    // batch kernel scratch: per-warp rejection masks
     // a8: L2 eviction-priority hints on the row copies: rows with id < hot_rows (the Zipf-hot
     // prefix) get evict_last if l2_hint & 1; the others evict_first if l2_hint & 2
     int64_t hot_rows;
@@ -70,7 +71,8 @@ cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T
 cudaError_t launch_init(float* M, int64_t V, int32_t D, int32_t Ds, uint64_t seed, int sms, cudaStream_t st);
 
 // batch.cu (a1 subsampling + window batching, a2 negative sampler)
-cudaError_t launch_batch(const StepParams& p, int sms, cudaStream_t st);
+size_t batch_redo_words(int sms);
+cudaError_t launch_batch(const StepParams& p, int sms, int blocks_per_sm, cudaStream_t st);
 
 // hogbatch_win.cu (window-resident rows; window <= 15)
 size_t win_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);

@@ -371,3 +371,20 @@ def test_rowpath_only_measurement_mode(w2v):
     w2v.set_option("rowpath_only", 1)
     with pytest.raises(w2v.W2VError):
         w2v.train(dev, ids.size, 1)
+
+
+def test_overlap_batch_option_same_results(w2v):
+    """Option overlap_batch (batch kernel of launch j+1 on a side stream, double-buffered batch
+    stream) changes nothing but timing: deterministic mode, several launches, bit-identical model
+    and stream to the serial order."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, cfg.n)
+    a = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, cfg.n),
+                opts={"launch_words": 3000, "overlap_batch": 0})
+    w2v.finalize()
+    b = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, cfg.n),
+                opts={"launch_words": 3000, "overlap_batch": 1})
+    assert a["stats"]["step_launches"] == b["stats"]["step_launches"] >= 6
+    for f in ("keep", "b", "N", "ctx", "neg"):
+        assert np.array_equal(a["dbg"][f], b["dbg"][f]), f
+    assert np.array_equal(a["M_in"], b["M_in"]) and np.array_equal(a["M_out"], b["M_out"])
