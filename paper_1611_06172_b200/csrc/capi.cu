@@ -162,10 +162,11 @@ int dmalloc(void** p, size_t bytes, const char* what) {
 
 // batch stream buffers for `chunks` chunks of Lp slots (batch.cu layout); the negatives are
 // padded by kSampGrp (8) targets because the step kernels prefetch a fixed group past nk
-int ensure_bt(int64_t chunks, int32_t Lp, int32_t KS) {
+int ensure_bt(int64_t chunks, int32_t Lp, int32_t KS, int sets) {
     const size_t nk = (size_t)chunks, kid = (size_t)chunks * Lp, neg = (size_t)chunks * Lp * KS + 8 * (size_t)KS;
     int rc;
-    for (auto& b : g.bt) {
+    for (int si = 0; si < sets; ++si) {
+        auto& b = g.bt[si];
         if (nk > b.cap_nk) {
             cudaFree(b.nk); b.nk = nullptr; b.cap_nk = 0;
             if ((rc = dmalloc((void**)&b.nk, nk * 4, "batch stream (kept counts)"))) return rc;
@@ -507,7 +508,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     if (g.algorithm == 1)
         per = std::max<int64_t>(1, std::min<int64_t>(per, (1ll << 30) / ((int64_t)p.Lp * negs_per_slot * 4)));
     {
-        int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, negs_per_slot);
+        int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, negs_per_slot,
+                           g.overlap_batch ? 2 : 1);
         if (rc) return rc;
     }
     p.bt_redo = g.bt_redo;
@@ -549,7 +551,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
             for (int64_t a = ilo; a < ihi; a += per, ++jl) {
                 p.chunk_lo = a;
                 p.chunk_hi = std::min(ihi, a + per);
-                const int set = (int)(jl & 1);
+                const int set = ovl ? (int)(jl & 1) : 0;
                 use_set(p, set);
                 if (ovl) {  // a1 + a2 -> batch stream set `set`, once step jl-2 has consumed it
                     CU(cudaStreamWaitEvent(g.side, ev_sdone[set], 0));
