@@ -197,6 +197,19 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Every CUDA event of one w2v_train call; destroyed on every exit path (errors included).
+struct EventPool {
+    std::vector<cudaEvent_t> v;
+    cudaError_t make(cudaEvent_t* e, unsigned flags = cudaEventDefault) {
+        cudaError_t r = cudaEventCreateWithFlags(e, flags);
+        if (r == cudaSuccess) v.push_back(*e);
+        return r;
+    }
+    ~EventPool() {
+        for (auto e : v) cudaEventDestroy(e);
+    }
+};
+
 // C13 host plan
 struct Plan {
     int64_t S, lo, hi, start, end, J, I;
@@ -334,7 +347,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     cudaStream_t st = g.stream;
     int launches = 0;
     cudaEvent_t ev0, ev_h2d, ev_setup, ev_end;
-    CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev_h2d)); CU(cudaEventCreate(&ev_setup)); CU(cudaEventCreate(&ev_end));
+    EventPool pool;
+    CU(pool.make(&ev0)); CU(pool.make(&ev_h2d)); CU(pool.make(&ev_setup)); CU(pool.make(&ev_end));
     CU(cudaEventRecord(ev0, st));
     // ---- corpus placement
     const int32_t* ids = ids_in;
@@ -520,10 +534,10 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     // runs on the main one (the step kernel's slabs leave room for one batch block per SM)
     const bool ovl = g.overlap_batch != 0;
     cudaEvent_t ev_tables, ev_bdone[2], ev_sdone[2];
-    CU(cudaEventCreateWithFlags(&ev_tables, cudaEventDisableTiming));
+    CU(pool.make(&ev_tables, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
-        CU(cudaEventCreateWithFlags(&ev_bdone[i], cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&ev_sdone[i], cudaEventDisableTiming));
+        CU(pool.make(&ev_bdone[i], cudaEventDisableTiming));
+        CU(pool.make(&ev_sdone[i], cudaEventDisableTiming));
     }
     CU(cudaEventRecord(ev_tables, st));
     if (ovl) {
@@ -536,7 +550,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     std::vector<int> ev_kind;  // 0 step, 1 sync, 2 batch
     auto mark = [&](int kind) -> cudaError_t {
         cudaEvent_t e;
-        cudaError_t r = cudaEventCreate(&e);
+        cudaError_t r = pool.make(&e);
         if (r != cudaSuccess) return r;
         evs.push_back(e);
         ev_kind.push_back(kind);
@@ -556,7 +570,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 if (ovl) {  // a1 + a2 -> batch stream set `set`, once step jl-2 has consumed it
                     CU(cudaStreamWaitEvent(g.side, ev_sdone[set], 0));
                     cudaEvent_t b0, b1;
-                    CU(cudaEventCreate(&b0)); CU(cudaEventCreate(&b1));
+                    CU(pool.make(&b0)); CU(pool.make(&b1));
                     bev.push_back(b0); bev.push_back(b1);
                     CU(cudaEventRecord(b0, g.side));
                     CU(launch_batch(p, g.sms, 1, g.side));
@@ -615,11 +629,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         CU(cudaEventElapsedTime(&ms, bev[i], bev[i + 1]));
         g.st.ms_batch += ms;
     }
-    for (auto e : bev) cudaEventDestroy(e);
-    cudaEventDestroy(ev_tables);
-    for (int i = 0; i < 2; ++i) { cudaEventDestroy(ev_bdone[i]); cudaEventDestroy(ev_sdone[i]); }
-    for (auto e : evs) cudaEventDestroy(e);
-    cudaEventDestroy(ev0); cudaEventDestroy(ev_h2d); cudaEventDestroy(ev_setup); cudaEventDestroy(ev_end);
+    // (events are destroyed by `pool`)
     g.st.words += (int64_t)hs.words;
     g.st.targets += (int64_t)hs.targets;
     g.st.row_touches += (int64_t)hs.row_touches;
