@@ -176,10 +176,11 @@ def run_ours(args):
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", args.sync_period)
-    # C14 by default when N > 1: hot 10% of the rows averaged every interval, the rest every 16th
-    # (C14 and §10: C13's full 2.4 GB average per 2^20 words would dominate the step)
-    hot = args.sync_hot_rows if args.sync_hot_rows >= 0 else (cfg.V // 10 if world > 1 else 0)
-    cold = args.sync_cold_every if args.sync_cold_every > 0 else (16 if world > 1 else 1)
+    # C14 by default when N > 1: the hot 5% of the rows averaged every interval, the rest every
+    # 32nd and at the end (C14 and §10: C13's full 2.4 GB average per 2^20 words would
+    # dominate the step; the loss gate is tests/test_dist_gloo.py)
+    hot = args.sync_hot_rows if args.sync_hot_rows >= 0 else (cfg.V // 20 if world > 1 else 0)
+    cold = args.sync_cold_every if args.sync_cold_every > 0 else (32 if world > 1 else 1)
     w2v.set_option("sync_hot_rows", hot)      # 0 = C13 full averaging
     w2v.set_option("sync_cold_every", cold)
     w2v.set_option("kernel", args.kernel)
@@ -315,9 +316,9 @@ def main():
                     help="BASELINE.json config (3 = the headline workload; 4, 5 = the larger-tile / 4M-vocab ones)")
     ap.add_argument("--sync-period", type=int, default=SYNC_P, help="words per GPU between model averagings")
     ap.add_argument("--sync-hot-rows", type=int, default=-1,
-                    help="C14 hot prefix averaged every interval (0 = all rows, C13; -1 = V/10 when N > 1)")
+                    help="C14 hot prefix averaged every interval (0 = all rows, C13; -1 = V/20 when N > 1)")
     ap.add_argument("--sync-cold-every", type=int, default=0,
-                    help="C14 cold rows averaged every this many intervals (0 = 16 when N > 1)")
+                    help="C14 cold rows averaged every this many intervals (0 = 32 when N > 1)")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
                     help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")
     args = ap.parse_args()

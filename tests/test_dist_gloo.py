@@ -124,7 +124,7 @@ def _loss_worker(rank, world, port, outdir, hot_rows, cold_every):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    Vg, n = 2000, 240_000
+    Vg, n = 2000, 480_000
     ids = inputs.Corpus("iid", Vg, 1.0, 5).tokens(0, n, threads=1)
     c = oracle.counts(ids, Vg)
 
@@ -134,7 +134,7 @@ def _loss_worker(rank, world, port, outdir, hot_rows, cold_every):
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             t /= world
 
-    M_in, M_out, st, _ = odist.train_replica(ids, Vg, 32, 5, 5, 0.025, 1e-3, 11, 20, world, rank, 1 << 12,
+    M_in, M_out, st, _ = odist.train_replica(ids, Vg, 32, 5, 5, 0.025, 1e-3, 11, 20, world, rank, 1 << 11,
                                              average, counts_global=c, hot_rows=hot_rows, cold_every=cold_every)
     if rank == 0:
         held = inputs.Corpus("iid", Vg, 1.0, 5).tokens(n, 60_000, threads=1)
@@ -146,13 +146,15 @@ def _loss_worker(rank, world, port, outdir, hot_rows, cold_every):
 
 def test_hot_cold_averaging_loss_gate(tmp_path):
     """C14 changes the sync semantics (SURVEY.md §8(f) NEXT-2 "gate it on loss"): 4 oracle replicas
-    with the hot 10% of rows averaged every interval and the cold rows every 4th interval reach a
-    held-out SGNS loss within 1% of C13's full averaging."""
+    (58 sync intervals each) with the hot 10% of rows averaged every interval and the rest every
+    4th, and with the bench's N > 1 default (hot 5%, the rest every 32nd and at the end), reach a
+    held-out SGNS loss within 1% of C13's full averaging after every interval."""
     world = 4
     out = {}
-    for hot, every in ((0, 1), (200, 4)):
+    for hot, every in ((0, 1), (200, 4), (100, 32)):
         mp.start_processes(_loss_worker, args=(world, _free_port(), str(tmp_path), hot, every), nprocs=world,
                            join=True, start_method="spawn")
         out[(hot, every)] = float(np.load(os.path.join(tmp_path, f"loss_{hot}_{every}.npy")))
-    print(f"held-out loss/pair, 4 replicas: full average {out[(0, 1)]:.6f}, hot/cold {out[(200, 4)]:.6f}")
-    assert abs(out[(200, 4)] / out[(0, 1)] - 1) < 0.01
+    print("held-out loss/pair, 4 replicas: " + ", ".join(f"H={h} C={c}: {v:.6f}" for (h, c), v in out.items()))
+    for key in ((200, 4), (100, 32)):
+        assert abs(out[key] / out[(0, 1)] - 1) < 0.01, key
