@@ -183,6 +183,8 @@ def run_ours(args):
     cold = args.sync_cold_every if args.sync_cold_every > 0 else (32 if world > 1 else 1)
     w2v.set_option("sync_hot_rows", hot)      # 0 = C13 full averaging
     w2v.set_option("sync_cold_every", cold)
+    ovl = int(args.sync_overlap > 0)   # C15 only on request (unmeasured at N > 1)
+    w2v.set_option("sync_overlap", ovl)
     w2v.set_option("kernel", args.kernel)
     w2v.set_option("algorithm", 1 if args.algorithm == "alg1" else 0)
     stream = torch.cuda.current_stream()
@@ -264,9 +266,10 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config],
                        "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": args.sync_period if world > 1 else None,
-                       "sync": ("C13 full average every interval" if hot == 0 else
-                                f"C14: rows [0,{hot}) averaged every interval, the rest every {cold}th and at the end")
-                       if world > 1 else None,
+                       "sync": (("C13 full average every interval" if hot == 0 else
+                                 f"C14: rows [0,{hot}) averaged every interval, the rest every {cold}th and at the end")
+                                + ("; C15: each average in flight during the next interval, applied one interval late"
+                                   if ovl else "")) if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": f"no flush: corpus ({n_local * 4 / 1e9:.1f} GB) and model ({cfg.V * cfg.D * 8 / 1e9:.2f} GB) exceed the 126 MB L2",
                        "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1"}.get(last["kernel"]),
@@ -319,6 +322,7 @@ def main():
                     help="C14 hot prefix averaged every interval (0 = all rows, C13; -1 = V/20 when N > 1)")
     ap.add_argument("--sync-cold-every", type=int, default=0,
                     help="C14 cold rows averaged every this many intervals (0 = 32 when N > 1)")
+    ap.add_argument("--sync-overlap", type=int, default=0, help="C15 overlapped averaging (1 = on)")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
                     help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")
     args = ap.parse_args()

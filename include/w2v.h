@@ -80,6 +80,10 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          are averaged after every interval (default 0 = all rows, i.e. C13)
  *  "sync_cold_every"       C14: rows [H,V) only after every this many intervals and after the
  *                          last interval of each epoch (>=1; default 1)
+ *  "sync_overlap"          C15 (default 0): the rows due are snapshot and averaged
+ *                          on a communication stream while the next interval trains; their
+ *                          correction M += avg - snapshot is applied one interval late; the last
+ *                          interval of an epoch ends with the plain blocking mean
  *  "lr_quantum"            Q of C8 (>=1; default 10000)
  *  "allow_target_negative" 0/1 (R2; default 0)
  *  "debug_base","debug_len" record the batch stream (C5-C7) for global positions

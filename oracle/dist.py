@@ -42,10 +42,17 @@ def synced_rows(k: int, J: int, V: int, hot_rows: int = 0, cold_every: int = 1) 
 
 
 def train_replica(ids_global, V, D, window, K, alpha0, t, seed, L, W, r, P, average, epochs=1,
-                  prec="f64", counts_global=None, debug=None, lr_quantum=10_000, hot_rows=0, cold_every=1):
+                  prec="f64", counts_global=None, debug=None, lr_quantum=10_000, hot_rows=0, cold_every=1,
+                  overlap=False):
     """Run replica r of W on its shard. `average(M_in, M_out)` must replace both matrices by the
     mean over replicas (called after every interval when W > 1, with row-slice views of the
     matrices when C14 averages only the hot prefix). Returns (M_in, M_out, stats, dbg).
+
+    overlap=True is C15: the rows due after interval k are SNAPSHOT (S = C = M[rows]),
+    S is averaged while interval k+1 trains, and after interval k+1 the replica applies
+    M[rows] += S - C (the average's correction, one interval late). The last interval of an epoch
+    applies any pending correction and then replaces the whole model by the plain mean (C13), so
+    the replicas end identical.
     """
     from . import Debug
     n = ids_global.size
@@ -62,9 +69,26 @@ def train_replica(ids_global, V, D, window, K, alpha0, t, seed, L, W, r, P, aver
     shard = np.ascontiguousarray(ids_global[start:end])
     for e in range(epochs):
         iv = sync_intervals(n, L, W, r, P)
+        pending = None  # C15: (lo, hi, S_in, S_out, C_in, C_out) of the average in flight
         for k, (a, b) in enumerate(iv):
             train_range(prm, thr, Ptab, shard, start, start, end - start, e, a, b, M_in, M_out, st, dbg, prec)
-            if W > 1:
+            if W == 1:
+                continue
+            if not overlap:
                 for lo_r, hi_r in synced_rows(k, len(iv), V, hot_rows, cold_every):
                     average(M_in[lo_r:hi_r], M_out[lo_r:hi_r])
+                continue
+            if pending is not None:
+                lo_p, hi_p, s_in, s_out, c_in, c_out = pending
+                M_in[lo_p:hi_p] += s_in - c_in
+                M_out[lo_p:hi_p] += s_out - c_out
+                pending = None
+            if k == len(iv) - 1:
+                average(M_in, M_out)  # the epoch ends with the plain mean: identical replicas
+                continue
+            (lo_r, hi_r), = synced_rows(k, len(iv), V, hot_rows, cold_every)
+            s_in, s_out = M_in[lo_r:hi_r].copy(), M_out[lo_r:hi_r].copy()
+            c_in, c_out = s_in.copy(), s_out.copy()
+            average(s_in, s_out)  # in flight during interval k+1 on the GPU
+            pending = (lo_r, hi_r, s_in, s_out, c_in, c_out)
     return M_in, M_out, st.as_dict(), dbg

@@ -83,6 +83,9 @@ struct Ctx {
     int64_t sync_period = 1 << 20;
     int64_t sync_hot_rows = 0;   // C14: hot prefix averaged every interval (0 = all rows)
     int64_t sync_cold_every = 1; // C14: the other rows every this many intervals (and the last)
+    int sync_overlap = 0;        // C15: average in flight during the next interval (one late)
+    float *syS = nullptr, *syC = nullptr;  // C15 snapshot (averaged in place) and its copy
+    cudaStream_t comm_stream = nullptr;
     int64_t Q = 10000;
     int allow_tn = 0;
     int64_t dbg_base = 0, dbg_len = 0;
@@ -273,6 +276,7 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
     } g.K = K; g.alpha = alpha; g.t = subsample; g.seed = seed;
     CU(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&g.comm_stream, cudaStreamNonBlocking));
     g.stream = g.own_stream;
     int rc;
     if ((rc = dmalloc((void**)&g.M, (size_t)V * 2 * g.Ds * sizeof(float), "the model [M_in|M_out]"))) return rc;
@@ -304,6 +308,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "sync_period_words") { if (v < 1) return fail(W2V_EINVAL, "sync_period_words must be >= 1"); g.sync_period = v; }
     else if (k == "sync_hot_rows") { if (v < 0) return fail(W2V_EINVAL, "sync_hot_rows must be >= 0"); g.sync_hot_rows = v; }
     else if (k == "sync_cold_every") { if (v < 1) return fail(W2V_EINVAL, "sync_cold_every must be >= 1"); g.sync_cold_every = v; }
+    else if (k == "sync_overlap") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "sync_overlap must be 0/1"); g.sync_overlap = (int)v; }
     else if (k == "lr_quantum") { if (v < 1) return fail(W2V_EINVAL, "lr_quantum must be >= 1"); g.Q = v; }
     else if (k == "allow_target_negative") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "allow_target_negative must be 0/1"); g.allow_tn = (int)v; }
     else if (k == "debug_base") { if (v < 0) return fail(W2V_EINVAL, "debug_base must be >= 0"); g.dbg_base = v; }
@@ -545,6 +550,17 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         for (int i = 0; i < 2; ++i) CU(cudaEventRecord(ev_sdone[i], st));
     }
     std::vector<cudaEvent_t> bev;  // (start, end) pairs of the batch launches on the side stream
+    // C15 state: rows [0, pend_hi) of the model have an average in flight on the comm stream
+    cudaEvent_t ev_snap, ev_ar;
+    CU(pool.make(&ev_snap, cudaEventDisableTiming));
+    CU(pool.make(&ev_ar, cudaEventDisableTiming));
+    int64_t pend_hi = 0;
+    if (dp() && g.sync_overlap && !g.syS) {
+        const size_t bytes = (size_t)g.V * 2 * g.Ds * sizeof(float);
+        int rc;
+        if ((rc = dmalloc((void**)&g.syS, bytes, "C15 snapshot"))) return rc;
+        if ((rc = dmalloc((void**)&g.syC, bytes, "C15 snapshot copy"))) return rc;
+    }
     int64_t jl = 0;                // launch counter (buffer set = jl & 1)
     std::vector<cudaEvent_t> evs;
     std::vector<int> ev_kind;  // 0 step, 1 sync, 2 batch
@@ -595,8 +611,33 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 CU(mark(1));
                 const int64_t H = (g.sync_hot_rows <= 0 || g.sync_hot_rows >= g.V) ? g.V : g.sync_hot_rows;
                 const bool full = H == g.V || g.sync_cold_every <= 1 || (k + 1) % g.sync_cold_every == 0 || k == J - 1;
-                int rc = full ? sync_models() : sync_models(0, H);
-                if (rc) return rc;
+                if (!g.sync_overlap) {
+                    int rc = full ? sync_models() : sync_models(0, H);
+                    if (rc) return rc;
+                } else {
+                    // C15: apply the average in flight (its correction), then put this interval's
+                    // rows in flight; the last interval ends with the plain (blocking) mean
+                    const size_t rowf = (size_t)2 * g.Ds;
+                    if (pend_hi > 0) {
+                        CU(cudaStreamWaitEvent(st, ev_ar, 0));
+                        CU(launch_sync_apply(g.M, g.syS, g.syC, (size_t)pend_hi * rowf, g.sms, st));
+                        pend_hi = 0;
+                    }
+                    if (k == J - 1) {
+                        int rc = sync_models();
+                        if (rc) return rc;
+                    } else {
+                        const int64_t hi_r = full ? g.V : H;
+                        CU(launch_sync_snap(g.M, g.syS, g.syC, (size_t)hi_r * rowf, g.sms, st));
+                        CU(cudaEventRecord(ev_snap, st));
+                        CU(cudaStreamWaitEvent(g.comm_stream, ev_snap, 0));
+                        NC(g_nccl.allReduce(g.syS, g.syS, (size_t)hi_r * rowf, ncclFloat32, ncclAvg, g.comm,
+                                            g.comm_stream));
+                        CU(cudaEventRecord(ev_ar, g.comm_stream));
+                        pend_hi = hi_r;
+                        if (full) g.st.syncs += 1; else g.st.syncs_hot += 1;
+                    }
+                }
                 CU(mark(1));
             }
         }
@@ -746,7 +787,10 @@ int w2v_finalize(void) {
     cudaFree(g.M); cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
     cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
     cudaStreamSynchronize(g.side);
+    cudaStreamSynchronize(g.comm_stream);
     cudaStreamDestroy(g.side);
+    cudaStreamDestroy(g.comm_stream);
+    cudaFree(g.syS); cudaFree(g.syC);
     cudaStreamDestroy(g.own_stream);
     Ctx fresh;
     g = fresh;

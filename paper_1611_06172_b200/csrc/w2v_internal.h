@@ -87,6 +87,10 @@ int wg_max_ctas_per_sm(const StepParams& p);
 cudaError_t launch_wg(const StepParams& p, int ctas, cudaStream_t st);
 void wg_phase_report();  // (experiment builds with W2V_PHASE_TIMING)
 
+// sync.cu (C15 overlapped averaging)
+cudaError_t launch_sync_apply(float* M, const float* S, const float* C, size_t n, int sms, cudaStream_t st);
+cudaError_t launch_sync_snap(const float* M, float* S, float* C, size_t n, int sms, cudaStream_t st);
+
 // alg1.cu (Algorithm 1, the level-1 baseline)
 bool alg1_supported(int D, int K);
 size_t alg1_warp_bytes(int L);

@@ -120,7 +120,7 @@ def test_shard_plan_partitions():
         assert len(J) == 1
 
 
-def _loss_worker(rank, world, port, outdir, hot_rows, cold_every):
+def _loss_worker(rank, world, port, outdir, hot_rows, cold_every, overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -135,26 +135,33 @@ def _loss_worker(rank, world, port, outdir, hot_rows, cold_every):
             t /= world
 
     M_in, M_out, st, _ = odist.train_replica(ids, Vg, 32, 5, 5, 0.025, 1e-3, 11, 20, world, rank, 1 << 11,
-                                             average, counts_global=c, hot_rows=hot_rows, cold_every=cold_every)
+                                             average, counts_global=c, hot_rows=hot_rows, cold_every=cold_every,
+                                             overlap=overlap)
     if rank == 0:
         held = inputs.Corpus("iid", Vg, 1.0, 5).tokens(n, 60_000, threads=1)
         _, _, hs, _ = oracle.train(held, Vg, 32, 5, 5, 0.0, 1e-3, 12, 20, model=(M_in, M_out))
-        np.save(os.path.join(outdir, f"loss_{hot_rows}_{cold_every}.npy"), hs["loss_sum"] / hs["loss_pairs"])
+        np.save(os.path.join(outdir, f"loss_{hot_rows}_{cold_every}_{int(overlap)}.npy"), hs["loss_sum"] / hs["loss_pairs"])
+    # the replicas end identical (every protocol ends an epoch with a plain mean)
+    g = [torch.empty_like(torch.from_numpy(M_in)) for _ in range(world)]
+    dist.all_gather(g, torch.from_numpy(M_in))
+    assert all(torch.equal(x, g[0]) for x in g)
     dist.barrier()
     dist.destroy_process_group()
 
 
 def test_hot_cold_averaging_loss_gate(tmp_path):
-    """C14 changes the sync semantics (SURVEY.md §8(f) NEXT-2 "gate it on loss"): 4 oracle replicas
-    (58 sync intervals each) with the hot 10% of rows averaged every interval and the rest every
-    4th, and with the bench's N > 1 default (hot 5%, the rest every 32nd and at the end), reach a
-    held-out SGNS loss within 1% of C13's full averaging after every interval."""
+    """C14/C15 change the sync semantics (SURVEY.md §8(f) NEXT-2 "gate it on loss"): 4 oracle
+    replicas (58 sync intervals each) with the hot 10% of rows averaged every interval and the rest
+    every 4th, with the bench's N > 1 default (hot 5%, the rest every 32nd and at the end), and
+    with C15's one-interval-late (overlapped) averaging, reach a held-out SGNS loss within 1% of
+    C13's full averaging after every interval; replicas end identical."""
     world = 4
     out = {}
-    for hot, every in ((0, 1), (200, 4), (100, 32)):
-        mp.start_processes(_loss_worker, args=(world, _free_port(), str(tmp_path), hot, every), nprocs=world,
+    for hot, every, ovl in ((0, 1, False), (200, 4, False), (100, 32, False), (100, 32, True), (0, 1, True)):
+        mp.start_processes(_loss_worker, args=(world, _free_port(), str(tmp_path), hot, every, ovl), nprocs=world,
                            join=True, start_method="spawn")
-        out[(hot, every)] = float(np.load(os.path.join(tmp_path, f"loss_{hot}_{every}.npy")))
-    print("held-out loss/pair, 4 replicas: " + ", ".join(f"H={h} C={c}: {v:.6f}" for (h, c), v in out.items()))
-    for key in ((200, 4), (100, 32)):
-        assert abs(out[key] / out[(0, 1)] - 1) < 0.01, key
+        out[(hot, every, ovl)] = float(np.load(os.path.join(tmp_path, f"loss_{hot}_{every}_{int(ovl)}.npy")))
+    print("held-out loss/pair, 4 replicas: " + ", ".join(f"H={h} C={c} overlap={o}: {v:.6f}"
+                                                         for (h, c, o), v in out.items()))
+    for key in out:
+        assert abs(out[key] / out[(0, 1, False)] - 1) < 0.01, key

@@ -315,12 +315,13 @@ def test_cfg3_full_size_sampled_stream(w2v):
 
 
 # ------------------------------------------------------------------ data-parallel path --------
-@pytest.mark.parametrize("hot_rows,cold_every", [(0, 1), (100, 3)])
-def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every):
+@pytest.mark.parametrize("hot_rows,cold_every,overlap", [(0, 1, 0), (100, 3, 0), (100, 3, 1), (0, 1, 1)])
+def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap):
     """The DP code path (C13: n_local all-gather, histogram all-reduce, sync intervals, model
-    averaging via NCCL; C14: hot-prefix averaging with the cold rows every 3rd interval) on a
-    1-rank communicator must reproduce the plain run exactly (deterministic mode; mean of one
-    replica = identity), with the expected full and hot-only sync counts."""
+    averaging via NCCL; C14: hot-prefix averaging with the cold rows every 3rd interval; C15: the
+    average in flight on the comm stream and applied one interval late) on a 1-rank communicator
+    must reproduce the plain run exactly (deterministic mode; mean of one replica = identity),
+    with the expected full and hot-only sync counts."""
     cfg = inputs.CONFIGS[1]
     ids = cfg.corpus().tokens(0, cfg.n)
     plain = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
@@ -331,6 +332,7 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every):
     w2v.set_option("sync_period_words", 3000)
     w2v.set_option("sync_hot_rows", hot_rows)
     w2v.set_option("sync_cold_every", cold_every)
+    w2v.set_option("sync_overlap", overlap)
     w2v.dist_init(0, 1, w2v.dist_unique_id())
     w2v.train(torch.from_numpy(ids).cuda(), ids.size, 1)
     M_in = np.empty((cfg.V, cfg.D), np.float32); M_out = np.empty_like(M_in)

@@ -63,6 +63,10 @@ def one(so, tokens, opts, reps, vmod=0, config=3):
     w2v.init(V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     for k, v in opts.items():
+        if k == "dp1":  # (experiment) the data-parallel path on a 1-rank NCCL communicator
+            if v:
+                w2v.dist_init(0, 1, w2v.dist_unique_id())
+            continue
         w2v.set_option(k, v)
     best = None
     for _ in range(reps):
@@ -71,7 +75,8 @@ def one(so, tokens, opts, reps, vmod=0, config=3):
         if best is None or st["ms_step"] < best["ms_step"]:
             best = st
     w2v.finalize()
-    return {"words_per_s": tokens / (best["ms_step"] / 1e3), "ms_step": best["ms_step"],
+    return {"words_per_s": tokens / (best["ms_step"] / 1e3), "ms_step": best["ms_step"], "ms_sync": best["ms_sync"],
+            "ms_total": best["ms_total"], "syncs": best["syncs"], "syncs_hot": best["syncs_hot"],
             "row_GBps": best["bytes_row"] / (best["ms_step"] / 1e3) / 1e9, "ms_batch": best["ms_batch"],
             "l2_window_MB": best["l2_window_bytes"] / 2**20, "l2_carve_MB": best["l2_carve_bytes"] / 2**20}
 
