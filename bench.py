@@ -272,7 +272,7 @@ def run_ours(args):
                                    if ovl else "")) if world > 1 else None,
                        "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
                        "l2": f"no flush: corpus ({n_local * 4 / 1e9:.1f} GB) and model ({cfg.V * cfg.D * 8 / 1e9:.2f} GB) exceed the 126 MB L2",
-                       "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1"}.get(last["kernel"]),
+                       "units_per_sm": last["units_per_sm"], "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1"}.get(last["kernel"]),
                        "algorithm": "hogbatch" if args.algorithm == "hogbatch" else "alg1 (PAPER.md:37-63, level-1 baseline)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -57,6 +57,7 @@ typedef struct {
     int64_t l2_window_bytes; /* a8: bytes of the hot-row prefix under the persisting-L2 window  */
     int64_t l2_carve_bytes;  /* a8: persisting-L2 carve-out set for the last w2v_train (0 = off) */
     int64_t syncs_hot;       /* C14 averagings of the hot-row prefix only (syncs counts full ones) */
+    int64_t units_per_sm;    /* step-kernel work units (1-warp CTAs) resident per SM, last train   */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").

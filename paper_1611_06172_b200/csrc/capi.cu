@@ -512,6 +512,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
+    g.st.units_per_sm = ctas >= g.sms ? ctas / g.sms : 1;
     g.st.kernel = kern == 0 ? 4 : kern;  // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1
     CU(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);

@@ -22,6 +22,7 @@
 // HogBatch batches them into C = A·Bᵀ and the two update GEMMs; the
 // "write back at the end of the GEMM" is the scatter of a7.
 #include <cstdio>
+#include <cstdlib>
 
 #include "hogbatch_common.cuh"
 
@@ -39,12 +40,16 @@ __device__ unsigned long long g_phase[8];
 namespace {
 
 #ifndef W2V_MINB
-#define W2V_MINB 10  // resident 1-warp CTAs per SM the register budget is sized for (smem allows 10)
+#define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for (the packed
+                     // D=300 slab lets 11 fit in smem; the padded ones 10)
 #endif
 
 // CP2 = float2 columns per lane (lane owns d = 2*(lane + 32*c2) + {0,1}, D <= 64*CP2);
 // KP1MAX >= K+1 (register tile of the K+1 output rows).
-template <int CP2, int KP1MAX>
+// RSC: compile-time smem row stride of the slab (floats); 0 = padded to 64*CP2 (predicate-free).
+// The packed instance for the paper's D=300 (RSC=300) saves 20 floats per row — what lets an 11th
+// work unit fit per SM — at the cost of a predicate on each lane's last float2 column.
+template <int CP2, int KP1MAX, int RSC>
 __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int TI = 32 / KP1MAX;  // inputs per reduce-scatter tile
@@ -57,9 +62,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     int32_t* kid = reinterpret_cast<int32_t*>(wbase + 16);   // kept ids of the chunk
     int32_t* kinfo = kid + p.Lp;                              // (offset << 8) | b
     int32_t* rowid0 = kinfo + p.Lp;                           // 2 x RMAX: ctx ids, target, negatives
-    int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWin x KS sampled negatives
-    float* gs = reinterpret_cast<float*>(negs + kSampWin * KS);  // G of the target, [N][KP1MAX]
-    constexpr int RS = 64 * CP2;                             // padded smem row stride (floats)
+    int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWinRows x KS negatives ring
+    float* gs = reinterpret_cast<float*>(negs + kSampWinRows * KS);  // G of the target, [N][KP1MAX]
+    constexpr int RS = RSC > 0 ? RSC : 64 * CP2;             // smem row stride (floats)
+    const bool lastok = RS >= 64 * CP2 || 2 * lane + 64 * (CP2 - 1) < D;  // lane's last float2 column exists
     float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
     float* As = Bs + KP1MAX * RS;                             // 2*window rows: context
     const uint32_t rowbytes = (uint32_t)D * 4u;
@@ -87,7 +93,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         const int N = hi - lo;
         for (int i = lane; i < N; i += 32) rowid[i] = kid[lo + i + (lo + i >= m ? 1 : 0)];
         if (lane == 0) rowid[N] = kid[m];
-        const int32_t* ng = negs + (m % kSampWin) * KS;
+        const int32_t* ng = negs + (m % kSampWinRows) * KS;
         for (int k = lane; k < K; k += 32) rowid[N + 1 + k] = ng[k];
         return N;
     };
@@ -106,7 +112,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
         const int64_t rel = s - p.chunk_lo;
         W2V_T(long long t0 = clock64();)
-        load_chunk(p, rel, kid, kinfo, nk_s, negs, lane);
+        load_chunk<kSampWinRows>(p, rel, kid, kinfo, nk_s, negs, lane);
         cp_async_wait_all();
         __syncwarp();
         W2V_T(ph[0] += clock64() - t0;)
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             // targets up to >= m+9, so waiting for all groups but this one covers target m+1.
             if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kSampGrp) {
                 const int c = nk - samp_hi < kSampGrp ? nk - samp_hi : kSampGrp;
-                fetch_negs(p, rel, samp_hi, c, negs, lane);
+                fetch_negs<kSampWinRows>(p, rel, samp_hi, c, negs, lane);
                 samp_hi += c;
             }
             cp_async_commit();
@@ -185,7 +191,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) {
-                    bq[j][c] = *reinterpret_cast<const float2*>(Bs + j * RS + 2 * lane + 64 * c);
+                    bq[j][c] = (c < CP2 - 1 || lastok) ? *reinterpret_cast<const float2*>(Bs + j * RS + 2 * lane + 64 * c)
+                                                       : make_float2(0.f, 0.f);
                     dq[j][c] = make_float2(0.f, 0.f);
                 }
             const int tt = lane / KP1MAX, tj = lane - tt * KP1MAX;  // dot held after the reduce-scatter
@@ -203,7 +210,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                     const float* Ai = As + (i0 + t < N ? i0 + t : 0) * RS + 2 * lane;
                     float2 a[CP2];
 #pragma unroll
-                    for (int c = 0; c < CP2; ++c) a[c] = *reinterpret_cast<const float2*>(Ai + 64 * c);
+                    for (int c = 0; c < CP2; ++c)
+                        a[c] = (c < CP2 - 1 || lastok) ? *reinterpret_cast<const float2*>(Ai + 64 * c) : make_float2(0.f, 0.f);
 #pragma unroll
                     for (int j = 0; j < KP1MAX; ++j) {
                         float2 s2 = make_float2(0.f, 0.f);
@@ -239,7 +247,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 float* Ai = As + i * RS + 2 * lane;
                 float2 a[CP2];
 #pragma unroll
-                for (int c = 0; c < CP2; ++c) a[c] = *reinterpret_cast<const float2*>(Ai + 64 * c);
+                for (int c = 0; c < CP2; ++c)
+                    a[c] = (c < CP2 - 1 || lastok) ? *reinterpret_cast<const float2*>(Ai + 64 * c) : make_float2(0.f, 0.f);
                 float2 g2[KP1MAX];
 #pragma unroll
                 for (int j = 0; j < KP1MAX; ++j) {
@@ -255,14 +264,14 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                     float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int j = 0; j < KP1MAX; ++j) s2 = ffma2(g2[j], bq[j][c], s2);
-                    *reinterpret_cast<float2*>(Ai + 64 * c) = s2;
+                    if (c < CP2 - 1 || lastok) *reinterpret_cast<float2*>(Ai + 64 * c) = s2;
                 }
             }
 #pragma unroll
             for (int j = 0; j < KP1MAX; ++j)
 #pragma unroll
                 for (int c = 0; c < CP2; ++c)
-                    *reinterpret_cast<float2*>(Bs + j * RS + 2 * lane + 64 * c) = dq[j][c];
+                    if (c < CP2 - 1 || lastok) *reinterpret_cast<float2*>(Bs + j * RS + 2 * lane + 64 * c) = dq[j][c];
             }
 #endif  // W2V_ABL_NOCOMPUTE
             fence_proxy_async_smem();
@@ -339,11 +348,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 using KernelFn = void (*)(const StepParams);
 
 struct Inst {
-    int cp2, kp1;
+    int cp2, kp1, rs;  // rs: packed row stride (the instance serves D == rs only), 0 = padded
     KernelFn fn;
 };
 
-#define W2V_INST(C, KK) {C, KK, hogbatch_step_kernel<C, KK>}
+#define W2V_INST(C, KK) {C, KK, 0, hogbatch_step_kernel<C, KK, 0>}
 // (float2 columns per lane, max K+1) instantiations; register tile ~ 4*CP2*KP1MAX floats.
 const Inst kInst[] = {
     W2V_INST(1, 2), W2V_INST(1, 4), W2V_INST(1, 6), W2V_INST(1, 8), W2V_INST(1, 16), W2V_INST(1, 32),
@@ -352,6 +361,7 @@ const Inst kInst[] = {
     W2V_INST(4, 2), W2V_INST(4, 4), W2V_INST(4, 6), W2V_INST(4, 8),
     W2V_INST(5, 2), W2V_INST(5, 4), W2V_INST(5, 6), W2V_INST(5, 8),
     W2V_INST(8, 2), W2V_INST(8, 4), W2V_INST(8, 6),
+    {5, 6, 300, hogbatch_step_kernel<5, 6, 300>},  // the paper's D=300, K<=5, packed rows
 };
 // Supported envelope (w2v_init rejects the rest): ceil(D/64) float2 columns per lane times
 // the padded K+1 tile must be one of the rows above, i.e. D <= 64 with K <= 31; D <= 128 with
@@ -360,9 +370,13 @@ const Inst kInst[] = {
 
 const Inst* pick(int D, int K) {
     const int need = (D + 63) / 64, kp1 = K + 1;
+    const char* pad = getenv("W2V_SLAB_PAD");
+    const bool packed_ok = !(pad && pad[0] == '1');
+    for (const Inst& in : kInst)  // a packed instance made for exactly this D wins
+        if (packed_ok && in.rs == D && in.cp2 >= need && in.kp1 >= kp1) return &in;
     const Inst* best = nullptr;
     for (const Inst& in : kInst) {
-        if (in.cp2 < need || in.kp1 < kp1) continue;
+        if (in.rs != 0 || in.cp2 < need || in.kp1 < kp1) continue;
         if (!best || in.cp2 * in.kp1 < best->cp2 * best->kp1) best = &in;
     }
     return best;
@@ -387,17 +401,19 @@ void step_phase_report() {
 
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     // [mbarrier 8 B | nk 4 B][kid Lp][kinfo Lp][rowid 2 x (2w+K+1)][negs 32 x max(K,1)][G tiles x 32]
-    // [slab: KP1MAX B rows + 2w A rows, stride 64*CP2 fp32]
+    // [slab: KP1MAX B rows + 2w A rows, stride RS fp32]. RS = 64*CP2 (zero padding), or D for a
+    // packed instance (W2V_SLAB_PAD=1 forces the padded one; experiments).
     const Inst* in = pick(D, K);
     if (!in) return 0;
+    const int RS = in->rs > 0 ? in->rs : 64 * in->cp2;
     const int R = 2 * window + K + 1;
     const int TI = 32 / in->kp1;
     const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
     const int Lp = (L + 3) & ~3;
-    const size_t ids = 16 + (size_t)(2 * Lp + 2 * R + kSampWin * (K > 0 ? K : 1)) * 4 + gfl * 4;
-    const size_t off = (ids + 127) / 128 * 128;
+    const size_t ids = 16 + (size_t)(2 * Lp + 2 * R + kSampWinRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
+    const size_t off = (ids + 15) / 16 * 16;  // 16-B aligned slab (bulk copies); every byte counts
     if (slab_offset) *slab_offset = (int32_t)off;
-    return off + (size_t)(in->kp1 + 2 * window) * 64 * in->cp2 * 4;
+    return off + (size_t)(in->kp1 + 2 * window) * RS * 4;
 }
 
 int step_max_ctas_per_sm(const StepParams& p) {

@@ -9,6 +9,7 @@ namespace w2v {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSampWin = 32;  // ring of targets whose negatives are staged in smem
+constexpr int kSampWinRows = 16;  // hogbatch.cu's ring: it fetches at most 16 targets ahead
 constexpr int kSampGrp = 8;   // targets whose negatives are fetched together (one async group)
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -44,13 +45,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // negatives) into the warp's smem: kid / kinfo (Lp ints each, 16-B async copies), the kept count
 // nk, and the negatives of kept targets [0, kSampGrp) into the ring — one cp.async group.
 // Reading past nk (stale slots, or the next chunk's) is harmless: the buffers are padded.
+template <int RING = kSampWin>
 __device__ __forceinline__ void fetch_negs(const StepParams& p, int64_t rel, int m_lo, int cnt, int32_t* negs,
                                            int lane) {
     const int K = p.K;  // K > 0 here, so KS == K and a group of targets is contiguous
     const int32_t* src = p.bt_neg + (rel * p.Lp + m_lo) * K;
-    int32_t* dst = negs + (m_lo % kSampWin) * K;
+    int32_t* dst = negs + (m_lo % RING) * K;
     for (int u = lane; u < cnt * K; u += 32) cp_async4(dst + u, src + u);
 }
+template <int RING = kSampWin>
 __device__ __forceinline__ void load_chunk(const StepParams& p, int64_t rel, int32_t* kid, int32_t* kinfo,
                                            int32_t* nk_s, int32_t* negs, int lane) {
     const int q = p.Lp >> 2;
@@ -61,7 +64,7 @@ __device__ __forceinline__ void load_chunk(const StepParams& p, int64_t rel, int
         cp_async16(kinfo + 4 * i, si + i);
     }
     if (lane == 0) cp_async4(nk_s, p.bt_nk + rel);
-    if (p.K > 0) fetch_negs(p, rel, 0, kSampGrp, negs, lane);
+    if (p.K > 0) fetch_negs<RING>(p, rel, 0, kSampGrp, negs, lane);
     cp_async_commit();
 }
 

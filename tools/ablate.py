@@ -77,6 +77,8 @@ def one(so, tokens, opts, reps, vmod=0, config=3):
     w2v.finalize()
     return {"words_per_s": tokens / (best["ms_step"] / 1e3), "ms_step": best["ms_step"], "ms_sync": best["ms_sync"],
             "ms_total": best["ms_total"], "syncs": best["syncs"], "syncs_hot": best["syncs_hot"],
+            "units_per_sm": best["units_per_sm"],
+
             "row_GBps": best["bytes_row"] / (best["ms_step"] / 1e3) / 1e9, "ms_batch": best["ms_batch"],
             "l2_window_MB": best["l2_window_bytes"] / 2**20, "l2_carve_MB": best["l2_carve_bytes"] / 2**20}
 
