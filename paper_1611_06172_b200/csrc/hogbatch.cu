@@ -39,6 +39,8 @@ __device__ unsigned long long g_phase[8];
 
 namespace {
 
+constexpr int kSmemChunk = 256;  // chunks up to this many (padded) kept slots are staged in smem
+
 #ifndef W2V_MINB
 #define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for (the packed
                      // D=300 slab lets 11 fit in smem; the padded ones 10)
@@ -59,9 +61,13 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     int32_t* nk_s = reinterpret_cast<int32_t*>(wbase + 8);   // kept count of the chunk
     const int D = p.D, Ds = p.Ds, K = p.K, KP1 = K + 1, window = p.window, RMAX = 2 * window + KP1;
     const int KS = K > 0 ? K : 1;
-    int32_t* kid = reinterpret_cast<int32_t*>(wbase + 16);   // kept ids of the chunk
-    int32_t* kinfo = kid + p.Lp;                              // (offset << 8) | b
-    int32_t* rowid0 = kinfo + p.Lp;                           // 2 x RMAX: ctx ids, target, negatives
+    // kept ids / (offset << 8) | b of the chunk: staged in smem for short chunks; long ones (L >
+    // kSmemChunk) are read in place from the batch stream (global, generic loads), which keeps a
+    // unit's smem at the slab's size — at L = 1000 that is 8 KB, i.e. 3 more units per SM
+    const bool chunk_smem = p.Lp <= kSmemChunk;
+    int32_t* kid_s = reinterpret_cast<int32_t*>(wbase + 16);
+    const int Lps = chunk_smem ? p.Lp : 0;
+    int32_t* rowid0 = kid_s + 2 * Lps;                        // 2 x RMAX: ctx ids, target, negatives
     int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWinRows x KS negatives ring
     float* gs = reinterpret_cast<float*>(negs + kSampWinRows * KS);  // G of the target, [N][KP1MAX]
     constexpr int RS = RSC > 0 ? RSC : 64 * CP2;             // smem row stride (floats)
@@ -86,6 +92,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     double st_loss = 0.0, st_tail = 0.0;
 
     // ---- C6: context ids, target and its (already sampled) negatives of kept target m
+    const int32_t* kid = kid_s;    // set per chunk (smem or the batch stream)
+    const int32_t* kinfo = kid_s + Lps;
     auto gather_list = [&](int m, int nk, int32_t* rowid) -> int {
         const int b = kinfo[m] & 255;
         const int lo = m - b < 0 ? 0 : m - b;
@@ -112,7 +120,14 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
         const int64_t rel = s - p.chunk_lo;
         W2V_T(long long t0 = clock64();)
-        load_chunk<kSampWinRows>(p, rel, kid, kinfo, nk_s, negs, lane);
+        if (chunk_smem) {
+            kid = kid_s;
+            kinfo = kid_s + Lps;
+        } else {
+            kid = p.bt_kid + rel * p.Lp;
+            kinfo = p.bt_kinfo + rel * p.Lp;
+        }
+        load_chunk<kSampWinRows>(p, rel, chunk_smem ? kid_s : nullptr, kid_s + Lps, nk_s, negs, lane);
         cp_async_wait_all();
         __syncwarp();
         W2V_T(ph[0] += clock64() - t0;)
@@ -410,7 +425,8 @@ size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     const int TI = 32 / in->kp1;
     const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
     const int Lp = (L + 3) & ~3;
-    const size_t ids = 16 + (size_t)(2 * Lp + 2 * R + kSampWinRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
+    const int Lps = Lp <= kSmemChunk ? Lp : 0;  // long chunks are read from the batch stream in place
+    const size_t ids = 16 + (size_t)(2 * Lps + 2 * R + kSampWinRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 15) / 16 * 16;  // 16-B aligned slab (bulk copies); every byte counts
     if (slab_offset) *slab_offset = (int32_t)off;
     return off + (size_t)(in->kp1 + 2 * window) * RS * 4;

@@ -56,7 +56,7 @@ __device__ __forceinline__ void fetch_negs(const StepParams& p, int64_t rel, int
 template <int RING = kSampWin>
 __device__ __forceinline__ void load_chunk(const StepParams& p, int64_t rel, int32_t* kid, int32_t* kinfo,
                                            int32_t* nk_s, int32_t* negs, int lane) {
-    const int q = p.Lp >> 2;
+    const int q = kid ? p.Lp >> 2 : 0;  // kid == nullptr: the caller reads kid/kinfo from global
     const int4* sk = reinterpret_cast<const int4*>(p.bt_kid + rel * p.Lp);
     const int4* si = reinterpret_cast<const int4*>(p.bt_kinfo + rel * p.Lp);
     for (int i = lane; i < q; i += 32) {
