@@ -276,10 +276,17 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                     for (int c = 0; c < CP2; ++c) dq[j][c] = ffma2(g2[j], a[c], dq[j][c]);
 #pragma unroll
                 for (int c = 0; c < CP2; ++c) {
-                    float2 s2 = make_float2(0.f, 0.f);
+                    // ΔIn_i = Σ_j G_ij B_j: with many outputs and few columns (cfg4: 16 x 2) the
+                    // single FFMA2 chain is latency-bound, so it runs as NCH interleaved chains
+                    constexpr int NCH = (KP1MAX >= 8 && CP2 <= 2) ? 4 : 1;
+                    float2 s2[NCH];
 #pragma unroll
-                    for (int j = 0; j < KP1MAX; ++j) s2 = ffma2(g2[j], bq[j][c], s2);
-                    if (c < CP2 - 1 || lastok) *reinterpret_cast<float2*>(Ai + 64 * c) = s2;
+                    for (int h = 0; h < NCH; ++h) s2[h] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < KP1MAX; ++j) s2[j % NCH] = ffma2(g2[j], bq[j][c], s2[j % NCH]);
+#pragma unroll
+                    for (int h = 1; h < NCH; ++h) s2[0] = fadd2(s2[0], s2[h]);
+                    if (c < CP2 - 1 || lastok) *reinterpret_cast<float2*>(Ai + 64 * c) = s2[0];
                 }
             }
 #pragma unroll
