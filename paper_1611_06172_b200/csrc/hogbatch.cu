@@ -126,6 +126,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         } else {
             kid = p.bt_kid + rel * p.Lp;
             kinfo = p.bt_kinfo + rel * p.Lp;
+            if (lane == 0) {  // the chunk's kept list, read target by target below, into L2 now
+                bulk_prefetch_l2(kid, (uint32_t)p.Lp * 4u);
+                bulk_prefetch_l2(kinfo, (uint32_t)p.Lp * 4u);
+            }
         }
         load_chunk<kSampWinRows>(p, rel, chunk_smem ? kid_s : nullptr, kid_s + Lps, nk_s, negs, lane);
         cp_async_wait_all();

@@ -127,6 +127,10 @@ __device__ __forceinline__ void bulk_red_add_s2g_hint(float* gdst, const void* s
                  "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
                  : "memory");
 }
+// bring [gsrc, gsrc+bytes) into L2 ahead of use (bytes multiple of 16, 16-B aligned)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // all but the most recent bulk group complete
