@@ -92,6 +92,7 @@ struct Ctx {
     int l2_persist = 0;          // persisting-L2 window (measured harmful: the bulk copies ignore it)
     int l2_hint = 1;             // a8 cache-policy hints on the row copies (StepParams::l2_hint)
     int64_t l2_hot_rows = -1;    // hot prefix for the hints (-1 = auto)
+    int64_t l2_hot_rows_in = -1; // ... for the M_in (context) rows of the rows kernel (-1 = same)
     int64_t l2_window_rows = 0;  // hot-prefix rows under the persisting window (0 = auto)
     int64_t l2_carve_mb = 0;     // persisting-L2 carve-out, MB (0 = device maximum)
     int64_t l2_hit_pct = 100;    // hitRatio of the window, percent
@@ -315,6 +316,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "debug_len") { if (v < 0) return fail(W2V_EINVAL, "debug_len must be >= 0"); g.dbg_len = v; }
     else if (k == "l2_persist") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "l2_persist must be 0/1"); g.l2_persist = (int)v; }
     else if (k == "l2_hint") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "l2_hint out of [0,3]"); g.l2_hint = (int)v; }
+    else if (k == "l2_hot_rows_in") { if (v < -1) return fail(W2V_EINVAL, "l2_hot_rows_in must be >= -1"); g.l2_hot_rows_in = v; }
     else if (k == "l2_hot_rows") { if (v < -1) return fail(W2V_EINVAL, "l2_hot_rows must be >= -1"); g.l2_hot_rows = v; }
     else if (k == "l2_window_rows") { if (v < 0) return fail(W2V_EINVAL, "l2_window_rows must be >= 0"); g.l2_window_rows = v; }
     else if (k == "l2_carve_mb") { if (v < 0) return fail(W2V_EINVAL, "l2_carve_mb must be >= 0"); g.l2_carve_mb = v; }
@@ -476,6 +478,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.loss_tail_from = g.loss_tail_from;
     p.l2_hint = g.l2_hint;
     p.hot_rows = g.l2_hot_rows >= 0 ? g.l2_hot_rows : (int64_t)(64ll << 20) / ((int64_t)2 * g.Ds * 4);
+    p.hot_rows_in = g.l2_hot_rows_in >= 0 ? g.l2_hot_rows_in : p.hot_rows;
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
     p.dbg_a1neg = g.dbg_a1neg;

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 float* dst = r < N ? As + r * RS : Bs + (r - N) * RS;
 #ifndef W2V_ABL_NOGATHER
                 bulk_g2s_hint(dst, p.M + (size_t)id * 2 * Ds + (r < N ? 0 : Ds), rowbytes, mbar,
-                              id < p.hot_rows ? pol_hot : pol_cold);
+                              id < (r < N ? p.hot_rows_in : p.hot_rows) ? pol_hot : pol_cold);
 #else
                 (void)dst; (void)id;
 #endif
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 #endif
 #ifndef W2V_ABL_NOSCATTER
                 bulk_red_add_s2g_hint(p.M + (size_t)id * 2 * Ds + (r < N ? 0 : Ds), src, rowbytes,
-                                      id < p.hot_rows ? pol_hot : pol_cold);
+                                      id < (r < N ? p.hot_rows_in : p.hot_rows) ? pol_hot : pol_cold);
 #else
                 (void)src; (void)id;
 #endif

@@ -55,7 +55,8 @@ struct StepParams {
     uint32_t* bt_redo;    // batch kernel scratch: per-warp rejection masks
     // a8: L2 eviction-priority hints on the row copies: rows with id < hot_rows (the Zipf-hot
     // prefix) get evict_last if l2_hint & 1; the others evict_first if l2_hint & 2
-    int64_t hot_rows;
+    int64_t hot_rows;     // M_out rows (targets, negatives; and both halves in the window kernels)
+    int64_t hot_rows_in;  // M_in rows (contexts) in the rows kernel
     int32_t l2_hint;
     int32_t rowpath_only; // measurement mode: rows kernel without a4-a6 (zero deltas; model unchanged)
     int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)
