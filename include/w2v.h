@@ -96,7 +96,8 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "l2_hint"               a8 L2 eviction-priority hints on the row copies: bit 0 = evict_last
  *                          on the hot prefix, bit 1 = evict_first on the other rows (default 1)
  *  "l2_hot_rows"           hot prefix for l2_hint (-1 = the rows that fit 64 MB; default -1)
- *  "l2_hot_rows_in"        ... for the M_in (context) rows of the rows kernel (-1 = same)
+ *  "l2_hot_rows_in"        ... for the M_in (context) rows of the rows kernel (-1 = all rows:
+ *                          a chunk's next targets re-read them within microseconds)
  *  "l2_persist"            0/1 persisting-L2 access-policy window over the hot-row prefix
  *                          (default 0: measured harmful on B200, the bulk copies ignore it and
  *                          the carve-out only shrinks L2; profiles/r01_ablations.md §2)

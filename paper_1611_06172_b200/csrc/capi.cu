@@ -92,7 +92,7 @@ struct Ctx {
     int l2_persist = 0;          // persisting-L2 window (measured harmful: the bulk copies ignore it)
     int l2_hint = 1;             // a8 cache-policy hints on the row copies (StepParams::l2_hint)
     int64_t l2_hot_rows = -1;    // hot prefix for the hints (-1 = auto)
-    int64_t l2_hot_rows_in = -1; // ... for the M_in (context) rows of the rows kernel (-1 = same)
+    int64_t l2_hot_rows_in = -1; // ... for the M_in (context) rows of the rows kernel (-1 = all)
     int64_t l2_window_rows = 0;  // hot-prefix rows under the persisting window (0 = auto)
     int64_t l2_carve_mb = 0;     // persisting-L2 carve-out, MB (0 = device maximum)
     int64_t l2_hit_pct = 100;    // hitRatio of the window, percent
@@ -478,7 +478,9 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.loss_tail_from = g.loss_tail_from;
     p.l2_hint = g.l2_hint;
     p.hot_rows = g.l2_hot_rows >= 0 ? g.l2_hot_rows : (int64_t)(64ll << 20) / ((int64_t)2 * g.Ds * 4);
-    p.hot_rows_in = g.l2_hot_rows_in >= 0 ? g.l2_hot_rows_in : p.hot_rows;
+    // a chunk's context rows are re-read by its next targets within microseconds: all M_in rows
+    // get evict_last by default (profiles/r01_ablations.md §2)
+    p.hot_rows_in = g.l2_hot_rows_in >= 0 ? g.l2_hot_rows_in : g.V;
     p.dbg_base = g.dbg_base; p.dbg_len = g.dbg_len;
     p.dbg_keep = g.dbg_keep; p.dbg_b = g.dbg_b; p.dbg_N = g.dbg_N; p.dbg_ctx = g.dbg_ctx; p.dbg_neg = g.dbg_neg;
     p.dbg_a1neg = g.dbg_a1neg;
