@@ -1,7 +1,7 @@
 /*
  * w2v.h — C-ABI of libw2v.so, the B200-native HogBatch skip-gram negative-sampling SGD step
  * (arXiv 1611.06172). Citations: PAPER.md:L = /root/reference/PAPER.md line L; "Alg.1 l.k" =
- * PAPER.md line 38+k; C1..C13 and R1..R18 are the contract and readings in DESIGN.md §2-§3.
+ * PAPER.md line 38+k; C1..C15 and R1..R18 are the contract and readings in DESIGN.md §2-§3.
  *
  * Conventions for every call:
  *  - Returns int: W2V_OK (0) or a negative W2V_E* code; w2v_last_error() then describes it
