@@ -33,6 +33,8 @@ VARIANTS = {
     "noscatter": ["-DW2V_ABL_NOSCATTER"],
     "phase": ["-DW2V_PHASE_TIMING"],
     "fulltile": ["-DW2V_DOT_FULL_TILE"],
+    "minb9": ["-DW2V_MINB=9"],
+    "minb8": ["-DW2V_MINB=8"],
     "nohot16": ["-DW2V_ABL_NOHOT=16"],
     "nohot256": ["-DW2V_ABL_NOHOT=256"],
     "nohot4096": ["-DW2V_ABL_NOHOT=4096"],
