@@ -3,6 +3,7 @@
 // NCCL data-parallel layer (dlopen'd libnccl.so.2, reading R13, C13).
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys, no-ops without a tool
 
 #include <algorithm>
 #include <climits>
@@ -201,6 +202,12 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// NVTX range for the host-side phases of a call (SURVEY.md §5 tracing); pops on every exit path.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Every CUDA event of one w2v_train call; destroyed on every exit path (errors included).
 struct EventPool {
     std::vector<cudaEvent_t> v;
@@ -241,6 +248,7 @@ bool dp() { return g.comm != nullptr; }
 // model) by their mean over ranks
 int sync_models(int64_t row_lo = 0, int64_t row_hi = -1) {
     if (!dp()) return W2V_OK;
+    NvtxRange nvtx("a9 model average");
     if (row_hi < 0) row_hi = g.V;
     if (row_hi <= row_lo) return W2V_OK;
     NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.Ds, g.M + (size_t)row_lo * 2 * g.Ds,
@@ -340,6 +348,7 @@ int w2v_set_stream(void* s) {
 }
 
 int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
+    NvtxRange nvtx_train("w2v_train");
     if (!g.live) return fail(W2V_ESTATE, "w2v_train before w2v_init");
     if (epochs < 1) return fail(W2V_EINVAL, "w2v_train: epochs=%d must be >= 1", epochs);
     if (n < 0) return fail(W2V_EINVAL, "w2v_train: n_tokens < 0");
@@ -690,6 +699,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
 }
 
 int w2v_sync(void) {
+    NvtxRange nvtx_sync("w2v_sync");
     if (!g.live) return fail(W2V_ESTATE, "w2v_sync before w2v_init");
     int rc = sync_models();
     if (rc) return rc;
