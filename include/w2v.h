@@ -32,6 +32,7 @@ extern "C" {
 #define W2V_ENOMEM (-3)   /* device allocation failed; message names the requested bytes      */
 #define W2V_ECUDA  (-4)   /* CUDA runtime error                                               */
 #define W2V_ENCCL  (-5)   /* NCCL error or NCCL library not loadable                          */
+#define W2V_ENUMERIC (-6) /* the model holds NaN/Inf after w2v_train (option check_finite)     */
 
 typedef struct {
     int64_t words;        /* raw corpus tokens processed (R14: the unit of words/s)           */
@@ -109,6 +110,8 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *  "kernel"                0 auto (default), 1 per-target rows (hogbatch.cu),
  *                          2 window-resident rows (hogbatch_win.cu; window <= 15), 3 window-
  *                          resident warp-specialised (hogbatch_wg.cu; window <= 15)
+ *  "check_finite"          1 (default): scan the model for NaN/Inf after every w2v_train (one
+ *                          streaming pass, ~0.5 ms at cfg3) and return W2V_ENUMERIC if found
  *  "overlap_batch"         1: the a1/a2 batch kernel of launch j+1 runs on a side stream
  *                          concurrently with the step kernel of launch j (double-buffered batch
  *                          stream); 0 (default): serialised on the library stream — the

@@ -17,7 +17,7 @@ if not os.path.exists(_SO):
     raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
 _lib = ctypes.CDLL(_SO)
 
-OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5
+OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENUMERIC = 0, -1, -2, -3, -4, -5, -6
 
 
 class Stats(ctypes.Structure):

@@ -48,6 +48,7 @@ struct Nccl {
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     const char* (*getErrorString)(ncclResult_t) = nullptr;
     bool load() {
         if (h) return true;
@@ -60,6 +61,7 @@ struct Nccl {
         allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
         commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
         getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+        commGetAsyncError = (decltype(commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
         return getUniqueId && commInitRank && allReduce && commDestroy && getErrorString;
     }
 } g_nccl;
@@ -126,6 +128,7 @@ struct Ctx {
     } bt[2];
     uint32_t* bt_redo = nullptr;
     cudaStream_t side = nullptr;
+    int check_finite = 1;   // NaN/Inf scan of the model after every w2v_train (W2V_ENUMERIC)
     int overlap_batch = 0;  // option "overlap_batch" (measured slower on B200: DESIGN.md §8)
     // debug
     uint8_t *dbg_keep = nullptr, *dbg_b = nullptr, *dbg_N = nullptr;
@@ -255,6 +258,11 @@ int sync_models(int64_t row_lo = 0, int64_t row_hi = -1) {
                         (size_t)(row_hi - row_lo) * 2 * g.Ds, ncclFloat32, ncclAvg, g.comm, g.stream));
     if (row_lo == 0 && row_hi == g.V) g.st.syncs += 1;
     else g.st.syncs_hot += 1;
+    if (g_nccl.commGetAsyncError) {  // a peer that failed surfaces here instead of as a hang later
+        ncclResult_t ae = ncclSuccess;
+        NC(g_nccl.commGetAsyncError(g.comm, &ae));
+        NC(ae);
+    }
     return W2V_OK;
 }
 
@@ -333,6 +341,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
     else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
+    else if (k == "check_finite") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "check_finite must be 0/1"); g.check_finite = (int)v; }
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window) or 3 (window, warp-specialised)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
@@ -657,9 +666,15 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
             }
         }
     }
+    if (g.check_finite) {  // failure detection: a diverged model is an error
+        CU(launch_finite_check(g.M, (size_t)g.V * 2 * g.Ds, &g.info->nonfinite, g.sms, st));
+        ++launches;
+    }
     CU(cudaEventRecord(ev_end, st));
     DevStats hs{};
+    SetupInfo hend{};
     CU(cudaMemcpyAsync(&hs, g.dstats, sizeof hs, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(&hend, g.info, sizeof hend, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     step_phase_report();
     win_phase_report();
@@ -695,6 +710,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     g.st.loss_tail_pairs += (int64_t)hs.loss_tail_pairs;
     g.st.launches = launches;
     g.st.bytes_row = (int64_t)hs.row_touches * 4 * g.D * 2;
+    if (g.check_finite && hend.nonfinite)
+        return fail(W2V_ENUMERIC, "w2v_train: the model holds NaN/Inf after training (diverged; lower alpha)");
     return W2V_OK;
 }
 

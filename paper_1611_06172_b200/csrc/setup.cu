@@ -160,7 +160,25 @@ __global__ void init_kernel(float* __restrict__ M, int64_t V, int32_t D, int32_t
     }
 }
 
+// flag |= 1 if any element of M[0, n) is NaN or Inf (divergence check)
+__global__ void finite_kernel(const float4* __restrict__ M, size_t n4, int32_t* flag) {
+    int bad = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = M[i];
+        bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 }  // namespace
+
+cudaError_t launch_finite_check(const float* M, size_t n, int32_t* flag, int sms, cudaStream_t st) {
+    size_t b = (n / 4 + 255) / 256;
+    if (b > (size_t)sms * 8) b = (size_t)sms * 8;
+    if (b < 1) b = 1;
+    finite_kernel<<<(int)b, 256, 0, st>>>(reinterpret_cast<const float4*>(M), n / 4, flag);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_hist(const int32_t* ids, int64_t n, int64_t V, unsigned long long* counts, SetupInfo* info,
                         int sms, cudaStream_t st, int* launches) {

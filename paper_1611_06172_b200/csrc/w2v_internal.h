@@ -10,6 +10,7 @@ struct SetupInfo {
     uint64_t PV;       // P[V], total sampler mass (C3)
     int32_t gshift;    // guide-table bucket shift
     int32_t bad_id;    // 1 if an id outside [0,V) was seen
+    int32_t nonfinite; // 1 if the model holds a NaN/Inf after training (option check_finite)
     int64_t first_bad; // (unused by kernels; host diagnostics)
 };
 
@@ -69,6 +70,7 @@ cudaError_t launch_hist(const int32_t* ids, int64_t n, int64_t V, unsigned long 
 cudaError_t launch_tables(const unsigned long long* counts, int64_t V, int64_t T, float t, uint64_t* thr,
                           uint64_t* P, uint64_t* scratch, int32_t* G, int gbits, SetupInfo* info, cudaStream_t st,
                           int* launches);
+cudaError_t launch_finite_check(const float* M, size_t n, int32_t* flag, int sms, cudaStream_t st);
 cudaError_t launch_init(float* M, int64_t V, int32_t D, int32_t Ds, uint64_t seed, int sms, cudaStream_t st);
 
 // batch.cu (a1 subsampling + window batching, a2 negative sampler)

@@ -390,3 +390,20 @@ def test_overlap_batch_option_same_results(w2v):
     for f in ("keep", "b", "N", "ctx", "neg"):
         assert np.array_equal(a["dbg"][f], b["dbg"][f]), f
     assert np.array_equal(a["M_in"], b["M_in"]) and np.array_equal(a["M_out"], b["M_out"])
+
+
+def test_divergence_is_reported(w2v):
+    """Failure detection: a learning rate that blows the model up
+    makes w2v_train return W2V_ENUMERIC after its NaN/Inf scan; a sane run passes the scan."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, cfg.n)
+    dev = torch.from_numpy(ids).cuda()
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, 1e30, cfg.t, cfg.seed)
+    w2v.set_option("sentence_len", cfg.L)
+    with pytest.raises(w2v.W2VError) as ei:
+        w2v.train(dev, ids.size, 1)
+    assert ei.value.code == w2v.ENUMERIC
+    w2v.finalize()
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("sentence_len", cfg.L)
+    w2v.train(dev, ids.size, 1)

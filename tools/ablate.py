@@ -64,6 +64,7 @@ def one(so, tokens, opts, reps, vmod=0, config=3):
     dev = host.cuda()
     w2v.init(V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
+    w2v.set_option("check_finite", 0)  # ablation variants may compute on junk on purpose
     for k, v in opts.items():
         if k == "dp1":  # (experiment) the data-parallel path on a 1-rank NCCL communicator
             if v:
