@@ -123,6 +123,11 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          loss_tail_sum / loss_tail_pairs (default: never)
  *  "epochs_total"          E used by the alpha schedule when training is split over several
  *                          w2v_train calls (0 = the epochs argument of each call; default 0)
+ *  "epoch_base"            global index of this call's first epoch: the C1 RNG epoch field and
+ *                          the C8 schedule position (0..255; default 0). With epochs_total it
+ *                          makes checkpoint/resume exact: w2v_get_embeddings after epoch e,
+ *                          w2v_set_embeddings + epoch_base = e+1 later (deterministic mode:
+ *                          bit-identical to one uninterrupted call)
  * Unknown key or bad value -> EINVAL. */
 int w2v_set_option(const char* key, int64_t value);
 

@@ -101,6 +101,7 @@ struct Ctx {
     int64_t l2_hit_pct = 100;    // hitRatio of the window, percent
     int ctas_per_sm = 0;
     int32_t epochs_total = 0;
+    int32_t epoch_base = 0;  // RNG epoch field / schedule position of this call's first epoch (resume)
     int64_t launch_words = 1ll << 26;
     int64_t loss_tail_from = INT64_MAX;
     int kernel = 0;  // 0 auto, 1 per-target rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
@@ -345,6 +346,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window) or 3 (window, warp-specialised)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
+    else if (k == "epoch_base") { if (v < 0 || v > 255) return fail(W2V_EINVAL, "epoch_base out of [0,255]"); g.epoch_base = (int32_t)v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
     else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
     return W2V_OK;
@@ -597,7 +599,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         return cudaEventRecord(e, st);
     };
     for (int32_t e = 0; e < epochs; ++e) {
-        p.epoch = e;
+        p.epoch = g.epoch_base + e;  // C1 epoch field and C8 progress of the global epoch
         const int64_t J = dp() ? pl.J : 1;
         for (int64_t k = 0; k < J; ++k) {
             const int64_t ilo = dp() ? chunk_lo + k * pl.I : chunk_lo;

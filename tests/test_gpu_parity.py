@@ -407,3 +407,23 @@ def test_divergence_is_reported(w2v):
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     w2v.train(dev, ids.size, 1)
+
+
+def test_checkpoint_resume_is_exact(w2v):
+    """Checkpoint/resume: one 2-epoch call == epoch 0, checkpoint through
+    w2v_get_embeddings, a fresh context restored with w2v_set_embeddings and epoch 1 run with
+    epoch_base=1 (epochs_total=2 on both halves) — bit-identical in deterministic mode, and within
+    1e-5 of the 2-epoch fp64 oracle."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, 8000)
+    full = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, epochs=2)
+    w2v.finalize()
+    half = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, epochs=1,
+                   opts={"epochs_total": 2})
+    w2v.finalize()
+    rest = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, epochs=1,
+                   opts={"epochs_total": 2, "epoch_base": 1}, model=(half["M_in"], half["M_out"]))
+    assert np.array_equal(rest["M_in"], full["M_in"]) and np.array_equal(rest["M_out"], full["M_out"])
+    o_in, o_out, _, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                     epochs=2)
+    assert rel_l2(rest["M_in"], o_in) <= 1e-5 and rel_l2(rest["M_out"], o_out) <= 1e-5
