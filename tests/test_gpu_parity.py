@@ -314,6 +314,33 @@ def test_cfg3_full_size_sampled_stream(w2v):
     assert st["loss_sum"] / st["loss_pairs"] < math.log(2)
 
 
+def test_cfg4_full_size_sampled_stream(w2v):
+    """BASELINE cfg4 at full size (V=1M, D=128, 800M iid Zipf(1.07) tokens, window=8, K=15,
+    t=1e-5, L=1000 — the long-chunk path that reads kept lists in place from the batch stream) in
+    the bench's launch configuration: batch stream bit-exact with the oracle on sampled windows."""
+    cfg = inputs.CONFIGS[4]
+    ids = cfg.corpus().tokens(0, cfg.n)
+    wins = [(1000 * 123_457 + 11, 1500), (cfg.n - 1800, 1800)]
+    c = oracle.counts(ids, cfg.V)
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("sentence_len", cfg.L)
+    dev = torch.from_numpy(ids).cuda()
+    for base, ln in wins:
+        w2v.set_option("debug_base", base)
+        w2v.set_option("debug_len", ln)
+        w2v.train(dev, cfg.n, 1)
+        d = {"keep": np.zeros(ln, np.uint8), "b": np.zeros(ln, np.uint8), "N": np.zeros(ln, np.uint8),
+             "ctx": np.zeros((ln, 2 * cfg.window), np.int32), "neg": np.zeros((ln, cfg.K), np.int32)}
+        w2v.debug_batches(d["keep"], d["b"], d["N"], d["ctx"], d["neg"])
+        lo = base // cfg.L * cfg.L
+        hi = min(((base + ln + cfg.L - 1) // cfg.L) * cfg.L, cfg.n)
+        o = oracle.batches(ids[lo:hi], cfg.V, cfg.window, cfg.K, cfg.t, cfg.seed, cfg.L, (base, ln),
+                           counts_global=c, ids_base=lo, n_global=cfg.n)
+        assert_stream_equal(d, o)
+    st = w2v.get_stats()
+    assert st["units_per_sm"] >= 10 and st["loss_sum"] / st["loss_pairs"] < math.log(2) * (cfg.K + 1) / 2
+
+
 # ------------------------------------------------------------------ data-parallel path --------
 @pytest.mark.parametrize("hot_rows,cold_every,overlap", [(0, 1, 0), (100, 3, 0), (100, 3, 1), (0, 1, 1)])
 def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap):
