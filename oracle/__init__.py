@@ -27,7 +27,7 @@ def build(force: bool = False) -> None:
     for prec, real in (("f64", "double"), ("f32", "float")):
         so = _so(prec)
         if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
-            subprocess.check_call(["gcc", *CFLAGS, f"-DREAL={real}", _SRC, "-o", so, "-lm"])
+            subprocess.check_call(["gcc", *CFLAGS, f"-DREAL={real}", _SRC, "-o", so, "-lm", "-pthread"])
 
 
 class OrcParams(ctypes.Structure):
@@ -99,6 +99,10 @@ def lib(prec: str = "f64"):
                                       ctypes.c_int64, realp, realp, ctypes.POINTER(OrcStats),
                                       ctypes.POINTER(OrcDebug)]
         L.orc_average.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int64]
+        L.orc_train_range_hogwild.argtypes = [ctypes.POINTER(OrcParams), u64p, u64p, i32p, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                              ctypes.c_int64, ctypes.c_int64, realp, realp, ctypes.POINTER(OrcStats),
+                                              ctypes.c_int32]
         L.orc_real_size.restype = ctypes.c_int
         _libs[prec] = L
     return _libs[prec]
@@ -235,6 +239,17 @@ def train_range(prm: OrcParams, thr, P, ids, ids_base, shard_start, n_local, e, 
                                    ctypes.byref(dbg.c) if dbg is not None else None)
     if rc != 0:
         raise ValueError("orc_train_range: bad arguments")
+
+
+def train_range_hogwild(prm: OrcParams, thr, P, ids, ids_base, shard_start, n_local, e, chunk_lo, chunk_hi,
+                        M_in, M_out, stats: OrcStats, threads: int, prec="f64") -> None:
+    """CPU TIMING BASELINE ONLY: `threads` Hogwild threads over contiguous chunk slices of the
+    same model; the result depends on the interleaving — never a parity value."""
+    ids = np.ascontiguousarray(ids, np.int32)
+    lib(prec).orc_train_range_hogwild(ctypes.byref(prm), _p(thr, ctypes.c_uint64), _p(P, ctypes.c_uint64),
+                                      _p(ids, ctypes.c_int32), ids_base, ids.size, shard_start, n_local, e,
+                                      chunk_lo, chunk_hi, M_in.ctypes.data, M_out.ctypes.data, ctypes.byref(stats),
+                                      threads)
 
 
 def train(ids, V, D, window, K, alpha0, t, seed, L, epochs=1, prec="f64", lr_quantum=10_000,

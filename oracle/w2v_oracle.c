@@ -26,6 +26,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <pthread.h>
 
 #ifndef REAL
 #define REAL double
@@ -406,6 +407,56 @@ int orc_train_range(const orc_params* prm, const uint64_t* thr, const uint64_t* 
         }
     }
     free(kept_pos_off); free(ctx); free(outs); free(negs);
+    return 0;
+}
+
+/* CPU TIMING BASELINE ONLY (SURVEY.md §8(c) "--threads T Hogwild mode", §8(d)): T threads run
+ * orc_train_range on contiguous slices of [chunk_lo, chunk_hi) concurrently on the SAME model,
+ * with unsynchronised read-modify-writes — Hogwild as PAPER.md:34 describes it ("parallelized
+ * over threads without any additional change"). Not used for parity: the result depends on the
+ * interleaving. Statistics are summed over threads; no debug stream. */
+typedef struct {
+    const orc_params* prm;
+    const uint64_t *thr, *P;
+    const int32_t* ids;
+    int64_t ids_base, ids_len, shard_start, n_local, chunk_lo, chunk_hi;
+    int32_t e;
+    REAL *M_in, *M_out;
+    orc_stats st;
+} orc_thread_job;
+
+static void* orc_thread_main(void* arg) {
+    orc_thread_job* j = (orc_thread_job*)arg;
+    orc_train_range(j->prm, j->thr, j->P, j->ids, j->ids_base, j->ids_len, j->shard_start, j->n_local, j->e,
+                    j->chunk_lo, j->chunk_hi, j->M_in, j->M_out, &j->st, NULL);
+    return NULL;
+}
+
+int orc_train_range_hogwild(const orc_params* prm, const uint64_t* thr, const uint64_t* P, const int32_t* ids,
+                            int64_t ids_base, int64_t ids_len, int64_t shard_start, int64_t n_local, int32_t e,
+                            int64_t chunk_lo, int64_t chunk_hi, REAL* M_in, REAL* M_out, orc_stats* st,
+                            int32_t threads) {
+    orc_thread_job jobs[256];
+    pthread_t th[256];
+    int32_t t, T = threads < 1 ? 1 : threads > 256 ? 256 : threads;
+    for (t = 0; t < T; ++t) {
+        orc_thread_job* j = &jobs[t];
+        j->prm = prm; j->thr = thr; j->P = P; j->ids = ids; j->ids_base = ids_base; j->ids_len = ids_len;
+        j->shard_start = shard_start; j->n_local = n_local; j->e = e;
+        j->chunk_lo = chunk_lo + (chunk_hi - chunk_lo) * t / T;
+        j->chunk_hi = chunk_lo + (chunk_hi - chunk_lo) * (t + 1) / T;
+        j->M_in = M_in; j->M_out = M_out;
+        memset(&j->st, 0, sizeof j->st);
+        pthread_create(&th[t], NULL, orc_thread_main, j);
+    }
+    for (t = 0; t < T; ++t) {
+        pthread_join(th[t], NULL);
+        st->words += jobs[t].st.words;
+        st->targets += jobs[t].st.targets;
+        st->row_touches += jobs[t].st.row_touches;
+        st->loss_pairs += jobs[t].st.loss_pairs;
+        st->loss_sum += jobs[t].st.loss_sum;
+    }
     return 0;
 }
 

@@ -487,3 +487,31 @@ def test_average_examples():
     oracle.average(r1); oracle.average(r2)
     assert np.allclose(r1[0], r2[0], rtol=1e-15, atol=1e-15)
     assert np.allclose(r1[0], np.mean(r, axis=0), atol=1e-15)
+
+
+def test_threaded_hogwild_oracle_mode_counts():
+    """The oracle's threaded Hogwild mode (CPU timing baseline only): one thread
+    is the sequential run bit for bit; T threads process exactly the same batch stream (position-
+    keyed RNG), so words/targets/row_touches/loss_pairs match the sequential run and the loss is
+    close (the model interleaving differs)."""
+    cfg = inputs.CONFIGS[2]
+    n = 60_000
+    ids = cfg.corpus().tokens(0, n)
+    c = oracle.counts(ids, cfg.V)
+    thr, P = oracle.thresholds(c, n, cfg.t), oracle.sampler(c)
+    prm = oracle.make_params(cfg.V, 32, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, n)
+    nch = (n + cfg.L - 1) // cfg.L
+    res = {}
+    for T in (0, 1, 4):
+        mi, mo = oracle.init(cfg.V, 32, cfg.seed)
+        M_in, M_out = mi.astype(np.float64), mo.astype(np.float64)
+        st = oracle.OrcStats()
+        if T == 0:
+            oracle.train_range(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, st)
+        else:
+            oracle.train_range_hogwild(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, st, T)
+        res[T] = (M_in, M_out, st.as_dict())
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert res[4][2][k] == res[0][2][k], k
+    assert abs(res[4][2]["loss_sum"] / res[0][2]["loss_sum"] - 1) < 0.02
