@@ -26,6 +26,10 @@ namespace w2v {
 
 namespace {
 
+#ifndef W2V_A1_MINB
+#define W2V_A1_MINB 16  // resident warps per SM the register budget is sized for (<= 128 registers)
+#endif
+
 __device__ __forceinline__ float2 ld_relaxed2(const float* p) {
     float2 v;
     asm volatile("ld.relaxed.gpu.global.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
@@ -48,7 +52,7 @@ __device__ __forceinline__ float warp_dot(const float2 (&a)[CP2], const float2 (
 }
 
 template <int CP2, int KMAX>
-__global__ void __launch_bounds__(32) alg1_kernel(const StepParams p) {
+__global__ void __launch_bounds__(32, W2V_A1_MINB) alg1_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;

@@ -34,6 +34,8 @@ VARIANTS = {
     "phase": ["-DW2V_PHASE_TIMING"],
     "fulltile": ["-DW2V_DOT_FULL_TILE"],
     "minb9": ["-DW2V_MINB=9"],
+    "a1mb20": ["-DW2V_A1_MINB=20"],
+    "a1mb24": ["-DW2V_A1_MINB=24"],
     "minb8": ["-DW2V_MINB=8"],
     "nohot16": ["-DW2V_ABL_NOHOT=16"],
     "nohot256": ["-DW2V_ABL_NOHOT=256"],
