@@ -282,11 +282,18 @@ def run_ours(args):
         peak, peak_src = peaks()
         achieved = last["bytes_row"] / (last["ms_step"] / 1e3) / 1e9   # GB/s, algorithmic bytes
         traffic = None   # DRAM bytes per launch (ncu --set full capture, profiles/), scaled to this launch size
+        l2roof = None    # the binding resource per that capture: L2 slice (LTS) throughput
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof) and args.algorithm == "hogbatch" and args.kernel in (0, 1):
             tr = json.load(open(prof))
             if tr.get("config", 3) == args.config:  # the capture is of this workload and kernel
                 traffic = tr.get("dram_bytes_per_word") * n_local / max(last["step_launches"], 1)
+                if "lts_bytes_per_cycle" in tr:
+                    l2roof = {"bound": "l2 (LTS slice throughput, all sectors incl. cross-die)",
+                              "achieved": tr["lts_bytes_per_cycle"], "peak": tr["lts_cap_bytes_per_cycle"],
+                              "unit": "B/cycle (chip)", "frac": tr["lts_bytes_per_cycle"] / tr["lts_cap_bytes_per_cycle"],
+                              "source": f"ncu --set full capture {tr.get('source')} (profiles/); peak: "
+                                        + tr.get("lts_cap_source", "")}
         out = {
             "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -308,6 +315,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
                          "row_bytes_per_word": last["bytes_row"] / n_local,
                          "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)},
+            "roofline_l2": l2roof,
             "rowpath_roof": None if roof is None else {
                 "value": roof, "unit": "words/s", "frac": (n / (kern_max / 1e3)) / roof,
                 "how": "same step kernel, launch configuration and batch stream with a4-a6 skipped (zero "

@@ -57,10 +57,24 @@ def main(tag, csv_path, rep, bench_log):
     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
     dram_bytes = dram * mult
     words = int(os.environ.get("W2V_PROFILED_WORDS", str(1 << 26)))
+    # L2 slice (LTS) throughput of the capture: all LTS sectors / LTS cycles, chip-wide B/cycle —
+    # against the LTS cap /opt/skills/guides/B300_MICROARCH.md measures (~6300 B/cycle full-chip)
+    raw = subprocess.run(["ncu", "-i", rep, "-k", os.environ.get("W2V_NCU_KERNEL", "regex:hogbatch_step"), "--page",
+                          "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    rd = dict(zip(rr[0], rr[-1]))
+    lts_bpc = float(rd["lts__t_sectors.sum"]) * 32 / float(rd["lts__cycles_elapsed.avg"])
     traffic = {"dram_bytes_per_launch": dram_bytes, "words_per_launch": words,
                "dram_bytes_per_word": dram_bytes / words, "source": os.path.basename(rep), "round": tag,
                "algorithmic_bytes_per_word": bench["roofline"]["row_bytes_per_word"],
-               "config": int(os.environ.get("W2V_PROFILED_CONFIG", "3")), "kernel": "hogbatch_step (rows)"}
+               "config": int(os.environ.get("W2V_PROFILED_CONFIG", "3")), "kernel": "hogbatch_step (rows)",
+               "lts_bytes_per_cycle": lts_bpc}
+    cap = os.path.join(ROOT, "profiles", "l2cap.json")
+    if os.path.exists(cap):
+        c = json.load(open(cap))
+        traffic["lts_cap_bytes_per_cycle"] = c["bulk_gather_reduce_lts_B_per_cycle"]
+        traffic["lts_cap_source"] = ("measured: tools/l2cap.cu, L2-resident bulk gather + bulk reduce of 1200-B rows "
+                                     "(the step's access pattern), profiles/l2cap.json")
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     json.dump({k: {"value": v, "unit": u} for k, (v, u) in s.items()},
               open(os.path.join(ROOT, "profiles", f"{tag}_hogbatch_step_ncu.json"), "w"), indent=1)
