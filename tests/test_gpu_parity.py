@@ -454,3 +454,24 @@ def test_checkpoint_resume_is_exact(w2v):
     o_in, o_out, _, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
                                      epochs=2)
     assert rel_l2(rest["M_in"], o_in) <= 1e-5 and rel_l2(rest["M_out"], o_out) <= 1e-5
+
+
+def test_caller_stream_same_results(w2v):
+    """w2v_set_stream (the bench hands the library torch's current stream): work enqueued on a
+    caller's stream gives bit-identical deterministic results to the library's private stream."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, 6000)
+    a = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
+    w2v.finalize()
+    s = torch.cuda.Stream()
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("mode", 1)
+    w2v.set_option("sentence_len", cfg.L)
+    w2v.set_stream(s.cuda_stream)
+    dev = torch.from_numpy(ids).cuda()
+    torch.cuda.synchronize()
+    w2v.train(dev, ids.size, 1)
+    M_in = np.empty((cfg.V, cfg.D), np.float32)
+    w2v.get_embeddings(0, M_in)
+    assert np.array_equal(M_in, a["M_in"])
+    w2v.set_stream(None)

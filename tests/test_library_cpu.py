@@ -59,3 +59,13 @@ def test_dist_plan_matches_oracle_protocol(binding):
             assert binding.dist_shard(n, L, W, r) == (lo * L, min(hi * L, n))
     with pytest.raises(binding.W2VError):
         binding.dist_plan(10, 0, 1, 0, 5)
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: importing the binding with the CUDA library missing raises ImportError."""
+    import subprocess
+    import sys
+    env = dict(os.environ, W2V_LIBRARY=str(tmp_path / "missing" / "libw2v.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_1611_06172_b200.binding"], capture_output=True,
+                       text=True, env=env, cwd=ROOT, timeout=120)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr
