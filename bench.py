@@ -1,21 +1,35 @@
 #!/usr/bin/env python
 """Benchmark: words/sec of the HogBatch SGNS step on BASELINE.json cfg3 (V=1M, D=300, 800M
-planted Zipf(1.07) tokens, window=5, K=5, t=1e-4), 1..8 B200s, plus its gather/scatter HBM
-roofline fraction.
+planted Zipf(1.07) tokens, window=5, K=5, t=1e-4), 1..8 B200s, plus its rooflines.
 
 A step = one `w2v_train(corpus, n, 1)` call = every SURVEY.md §8(a) row over the whole corpus
-(setup a0, subsampling/window a1, sampler a2, fused step a3-a7, L2 window a8, and with N>1 the
+(setup a0, subsampling/window a1, sampler a2, fused step a3-a7, L2 hints a8, and with N>1 the
 model averaging a9 every 2^20 words per GPU). `value` is device-timed (CUDA events on the
 library's stream, max over ranks) with the corpus resident in HBM; `e2e` is the same call with a
 pinned HOST corpus (H2D inside the timed region). `--impl reference` times the CPU oracle.
+
+Rooflines, every denominator measured in this run except HBM's:
+  roofline       the BINDING resource, the L2 row path: algorithmic row bytes B_row of the timed
+                 calls / step-kernel time, against the in-run cap of the same access pattern
+                 (tools/peaks.cu peaks_l2_rowpath: bulk gather + bulk reduce of the model's rows,
+                 L2-resident, all SMs);
+  roofline_hbm   BASELINE.json's "fraction of gather/scatter HBM roofline": the same B_row rate
+                 against the measured HBM copy bandwidth (MEASURED_PEAKS.json). It exceeds 1
+                 because L2 serves the Zipf-hot rows; DRAM bytes actually moved are in `traffic`;
+  roofline_cache the survey's cache-aware bound T_roof = max(B_row/BW_L2, B_cold/BW_HBM,
+                 FLOP/FMA_peak) over the measured step-kernel time;
+  fma            the FMA-pipe share: 6·D·loss_pairs FLOP / step-kernel time vs the in-run FFMA2
+                 peak (tools/peaks.cu peaks_ffma2).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -39,8 +53,9 @@ WORKLOADS = {
        "on-device (L=1000), 1 epoch per step",
 }
 SYNC_P = 1 << 20
-REF_SAMPLE = 1 << 17      # raw words per reference step (bounded CPU sample of cfg3)
-BASE_SAMPLE = 1 << 19     # raw words for the cpu_baseline leg
+REF_SAMPLE = 1 << 17      # raw words per thread per reference step (bounded CPU sample of cfg3)
+BASE_SAMPLE = 1 << 19     # raw words per thread for the cpu_baseline leg
+PEAKS_SO = os.path.join(ROOT, "tools", "libw2v_peaks.so")
 
 
 def peaks():
@@ -49,6 +64,37 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` object of BOTH arms (ours and --impl reference): the workload, not the run."""
+    cfg = inputs.CONFIGS[args.config]
+    n = args.tokens if args.tokens else cfg.n
+    hot, cold = sync_scheme(args, cfg, world)
+    return {"workload": WORKLOADS[args.config], "V": cfg.V, "D": cfg.D, "window": cfg.window, "K": cfg.K,
+            "t": cfg.t, "n_tokens": n, "full_size": n == cfg.n, "epochs_per_step": 1,
+            "sync_period_words": args.sync_period if world > 1 else None,
+            "sync": sync_name(hot, cold, args.sync_overlap > 0) if world > 1 else None,
+            "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
+            "l2": "no flush: corpus (3.2 GB) and model (2.4 GB) exceed the 126 MB L2" if args.config != 5 else
+                  "no flush: corpus (32 GB) and model (9.6 GB) exceed the 126 MB L2",
+            "algorithm": "hogbatch" if args.algorithm == "hogbatch" else "alg1 (PAPER.md:37-63, level-1 baseline)"}
+
+
+def sync_scheme(args, cfg, world):
+    """C13 (the paper's protocol, BASELINE cfg3: full-model average every 2^20 words per GPU) is
+    the default; C14 hot/cold is opt-in (--sync-hot-rows H --sync-cold-every C)."""
+    hot = max(args.sync_hot_rows, 0) if world > 1 else 0
+    cold = max(args.sync_cold_every, 1) if world > 1 else 1
+    return hot, cold
+
+
+def sync_name(hot, cold, ovl):
+    s = ("C13: full-model allreduce average (ncclAvg) after every interval" if hot == 0 or cold <= 1 else
+         f"C14: rows [0,{hot}) averaged every interval, the rest every {cold}th and at the end")
+    if ovl:
+        s += "; C15: each average in flight (out-of-place) during the next interval, applied one interval late"
+    return s
 
 
 class Clocks:
@@ -94,22 +140,6 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def _oracle_setup(cfg, sample):
-    import oracle
-    ids = cfg.corpus().tokens(0, sample)
-    c = oracle.counts(ids, cfg.V)
-    thr, P = oracle.thresholds(c, sample, cfg.t), oracle.sampler(c)
-    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, sample)
-    return ids, thr, P, prm
-
-
-def _oracle_model(cfg):
-    import oracle
-    mi, mo = oracle.init(cfg.V, cfg.D, cfg.seed)
-    M_in, M_out = mi.astype(np.float64), mo.astype(np.float64)
-    return M_in, M_out
-
-
 def host_threads() -> int:
     try:
         return max(1, len(os.sched_getaffinity(0)))
@@ -117,62 +147,108 @@ def host_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def _oracle_time(cfg, n, threads, prec, reps=1, warm=0):
+    """Seconds for `reps` Hogwild-threaded oracle passes over the first n raw words of cfg (setup
+    excluded; a fresh contract-init model; threads = 1 runs the sequential O-HB)."""
+    import oracle
+    ids = cfg.corpus().tokens(0, n)
+    c = oracle.counts(ids, cfg.V)
+    thr, P = oracle.thresholds(c, n, cfg.t), oracle.sampler(c)
+    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, n)
+    mi, mo = oracle.init(cfg.V, cfg.D, cfg.seed)
+    dt = oracle.real_dtype(prec)
+    M_in, M_out = mi.astype(dt), mo.astype(dt)
+    del mi, mo
+    nch = (n + cfg.L - 1) // cfg.L
+    for _ in range(warm):
+        oracle.train_range_hogwild(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, oracle.OrcStats(), threads, prec)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        if threads == 1:
+            oracle.train_range(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, oracle.OrcStats(), None, prec)
+        else:
+            oracle.train_range_hogwild(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, oracle.OrcStats(), threads,
+                                       prec)
+    return time.perf_counter() - t0
+
+
 def cpu_baseline(cfg, sample):
-    """The oracle as it stands on the box's host cores: its Hogwild threaded mode over all cores
-    (the paper's CPU setting) on `threads` x `sample` raw words, plus
-    the sequential fp64 O-HB on `sample` words as `value_1core`; setup excluded."""
+    """The oracle on the box's host cores: its Hogwild threaded mode
+    ("parallelized over threads without any additional change") over all host
+    threads, fp32 (the GPU path's precision) built -O3 -march=native for this host; plus the
+    same in fp64 (-O2, the parity build) and the sequential fp64 O-HB on one core. Setup excluded.
+    A deliberately simple program: the GPU/CPU ratio says nothing about kernel quality."""
     import oracle
     T = host_threads()
-    ids, thr, P, prm = _oracle_setup(cfg, sample * T)
+    flags = oracle.build_native()
     n = sample * T
-    prm = oracle.make_params(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, 1, n)
-    M_in, M_out = _oracle_model(cfg)
-    nch = (n + cfg.L - 1) // cfg.L
-    t0 = time.perf_counter()
-    oracle.train_range_hogwild(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, oracle.OrcStats(), T)
-    dt_t = time.perf_counter() - t0
-    del M_in, M_out
-    M_in, M_out = _oracle_model(cfg)
-    nch1 = (sample + cfg.L - 1) // cfg.L
-    t0 = time.perf_counter()
-    oracle.train_range(prm, thr, P, ids, 0, 0, n, 0, 0, nch1, M_in, M_out, oracle.OrcStats())
-    dt_1 = time.perf_counter() - t0
-    return {"value": n / dt_t, "unit": "words/s", "cores": T, "kind": "oracle",
-            "sample": f"first {n} raw words of cfg{cfg.idx} (V={cfg.V}, D={cfg.D}), fp64 O-HB in the oracle's "
+    dt32 = _oracle_time(cfg, n, T, "f32native")
+    dt64 = _oracle_time(cfg, n, T, "f64")
+    dt1 = _oracle_time(cfg, sample, 1, "f64")
+    return {"value": n / dt32, "unit": "words/s", "cores": T, "kind": "oracle",
+            "sample": f"first {n} raw words of cfg{cfg.idx} (V={cfg.V}, D={cfg.D}), fp32 O-HB in the oracle's "
                       f"Hogwild threaded mode on {T} host threads, setup excluded",
-            "seconds": dt_t, "value_1core": sample / dt_1,
-            "sample_1core": f"first {sample} raw words, sequential fp64 O-HB, 1 thread ({dt_1:.1f} s)"}
+            "seconds": dt32, "cpu_model": cpu_model(), "nproc": os.cpu_count(), "threads": T,
+            "compiler": f"gcc {flags}",
+            "value_fp64": n / dt64, "compiler_fp64": "gcc " + " ".join(oracle.CFLAGS) + " -DREAL=double",
+            "value_1core": sample / dt1,
+            "sample_1core": f"first {sample} raw words, sequential fp64 O-HB, 1 thread ({dt1:.1f} s)"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg = inputs.CONFIGS[CFG]
+    cfg = inputs.CONFIGS[args.config]
     import oracle
     T = host_threads()
+    flags = oracle.build_native()
     n = REF_SAMPLE * T
-    ids, thr, P, prm = _oracle_setup(cfg, n)
-    M_in, M_out = _oracle_model(cfg)
-    nch = (n + cfg.L - 1) // cfg.L
-    for _ in range(args.warmup):
-        oracle.train_range_hogwild(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, oracle.OrcStats(), T)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.train_range_hogwild(prm, thr, P, ids, 0, 0, n, 0, 0, nch, M_in, M_out, oracle.OrcStats(), T)
-    dt = time.perf_counter() - t0
+    dt = _oracle_time(cfg, n, T, "f32native", reps=args.steps, warm=args.warmup)
     v = n * args.steps / dt
-    sample = (f"first {n} raw words of cfg3 per step, fp64 oracle (O-HB) in its Hogwild threaded mode on "
-              f"{T} host threads")
+    sample = (f"first {n} raw words of cfg{cfg.idx} per step (a bounded sample of the workload), fp32 oracle "
+              f"(O-HB) in its Hogwild threaded mode on {T} host threads, gcc {flags}")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "words/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3 (bounded CPU sample)", "V": cfg.V, "D": cfg.D, "window": cfg.window,
-                   "K": cfg.K, "t": cfg.t, "sample_words": n},
-        "cpu_baseline": {"value": v, "unit": "words/s", "cores": T, "kind": "oracle", "sample": sample},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": v, "unit": "words/s", "cores": T, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": v, "unit": "words/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
     return 0
+
+
+def measure_caps(row_bytes, rows_per_target, units_per_sm):
+    """In-run roofline denominators (tools/peaks.cu): the L2 row-path cap of this access pattern
+    (max over a few residencies, R = rows per target) and the FFMA2 peak. None if unavailable."""
+    if not os.path.exists(PEAKS_SO):
+        return None
+    lib = ctypes.CDLL(PEAKS_SO)
+    d = ctypes.c_double(0.0)
+    caps = {}
+    for w in sorted({units_per_sm, 8, 12, 16}):
+        if lib.peaks_l2_rowpath(int(row_bytes), int(rows_per_target), int(w), ctypes.byref(d)) == 0:
+            caps[w] = d.value
+    out = {"l2_rowpath_gbs": max(caps.values()) if caps else None, "l2_rowpath_by_units": caps}
+    if lib.peaks_ffma2(ctypes.byref(d)) == 0:
+        out["ffma2_tflops"] = d.value
+    if lib.peaks_l2_read(ctypes.byref(d)) == 0:
+        out["l2_read_gbs"] = d.value
+    if lib.peaks_l2_red(ctypes.byref(d)) == 0:
+        out["l2_red_gbs"] = d.value
+    return out
 
 
 def run_ours(args):
@@ -186,6 +262,7 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator lines (nRanks) for the driver's log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = inputs.CONFIGS[args.config]
     n = args.tokens if args.tokens else cfg.n      # --tokens: profiling only (prefix of the config)
@@ -203,14 +280,10 @@ def run_ours(args):
     w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
     w2v.set_option("sentence_len", cfg.L)
     w2v.set_option("sync_period_words", args.sync_period)
-    # C14 by default when N > 1: the hot 5% of the rows averaged every interval, the rest every
-    # 32nd and at the end (C14 and §10: C13's full 2.4 GB average per 2^20 words would
-    # dominate the step; the loss gate is tests/test_dist_gloo.py)
-    hot = args.sync_hot_rows if args.sync_hot_rows >= 0 else (cfg.V // 20 if world > 1 else 0)
-    cold = args.sync_cold_every if args.sync_cold_every > 0 else (32 if world > 1 else 1)
-    w2v.set_option("sync_hot_rows", hot)      # 0 = C13 full averaging
+    hot, cold = sync_scheme(args, cfg, world)
+    w2v.set_option("sync_hot_rows", hot)      # 0 = C13 full averaging (default)
     w2v.set_option("sync_cold_every", cold)
-    ovl = int(args.sync_overlap > 0)   # C15 only on request (unmeasured at N > 1)
+    ovl = int(args.sync_overlap > 0)
     w2v.set_option("sync_overlap", ovl)
     w2v.set_option("kernel", args.kernel)
     w2v.set_option("algorithm", 1 if args.algorithm == "alg1" else 0)
@@ -230,6 +303,12 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def maxr(*vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
+
     for _ in range(args.warmup):
         w2v.train(dev, n_local, 1)
     barrier()
@@ -244,90 +323,108 @@ def run_ours(args):
         barrier()
     ms = e0.elapsed_time(e1)
     ms_step_kernel = sum(s["ms_step"] for s in steps) / len(steps)
-    t = torch.tensor([ms, ms_step_kernel], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_max = float(t[0]), float(t[1])
+    ms_max, kern_max = maxr(ms, ms_step_kernel)
     value = n * args.steps / (ms_max / 1e3)
 
-    # e2e: the same call with a pinned HOST corpus (H2D + stats D2H inside the timed region)
-    e2e_steps = max(1, min(args.steps, 3))
+    # e2e: the same call, every timed step, with a pinned HOST corpus (H2D inside) and the
+    # step's statistics (loss) read back to the host
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(e2e_steps):
+    for _ in range(args.steps):
         w2v.train(host, n_local, 1)
+        w2v.get_stats()
     f1.record(stream)
     barrier()
-    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = n * e2e_steps / (float(te[0]) / 1e3)
+    te, = maxr(f0.elapsed_time(f1))
+    e2e_value = n * args.steps / (te / 1e3)
     last = steps[-1]
 
     # row-path roof: the same kernel and batch stream with a4-a6 skipped (zero deltas reduced,
     # model unchanged) — what the gathers + scatters alone sustain on this chip
     roof = None
-    if args.algorithm == "hogbatch" and args.kernel in (0, 1):
+    if args.algorithm == "hogbatch" and args.kernel in (0, 1, 4) and not args.no_rowpath:
         w2v.set_option("rowpath_only", 1)
         w2v.train(dev, n_local, 1)
         rs = w2v.get_stats()
         w2v.set_option("rowpath_only", 0)
-        tr = torch.tensor([rs["ms_step"]], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
-        roof = n / (float(tr[0]) / 1e3)
+        tr, = maxr(rs["ms_step"])
+        roof = n / (tr / 1e3)
 
     if rank == 0:
         peak, peak_src = peaks()
-        achieved = last["bytes_row"] / (last["ms_step"] / 1e3) / 1e9   # GB/s, algorithmic bytes
+        kern_s = last["ms_step"] / 1e3
+        bps = last["bytes_row"] / kern_s                       # algorithmic row bytes / s
+        rows_per_target = last["row_touches"] / max(last["targets"], 1)
+        caps = measure_caps(4 * cfg.D, max(1, round(rows_per_target)), last["units_per_sm"])
         traffic = None   # DRAM bytes per launch (ncu --set full capture, profiles/), scaled to this launch size
-        l2roof = None    # the binding resource per that capture: L2 slice (LTS) throughput
+        traffic_src = None
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(prof) and args.algorithm == "hogbatch" and args.kernel in (0, 1):
+        if os.path.exists(prof) and args.algorithm == "hogbatch":
             tr = json.load(open(prof))
-            if tr.get("config", 3) == args.config:  # the capture is of this workload and kernel
+            if tr.get("config", 3) == args.config and tr.get("kernel_id", last["kernel"]) == last["kernel"]:
                 traffic = tr.get("dram_bytes_per_word") * n_local / max(last["step_launches"], 1)
-                if "lts_bytes_per_cycle" in tr:
-                    l2roof = {"bound": "l2 (LTS slice throughput, all sectors incl. cross-die)",
-                              "achieved": tr["lts_bytes_per_cycle"], "peak": tr["lts_cap_bytes_per_cycle"],
-                              "unit": "B/cycle (chip)", "frac": tr["lts_bytes_per_cycle"] / tr["lts_cap_bytes_per_cycle"],
-                              "source": f"ncu --set full capture {tr.get('source')} (profiles/); peak: "
-                                        + tr.get("lts_cap_source", "")}
+                traffic_src = f"ncu --set full capture {tr.get('source')} ({tr.get('round')}), profiles/ncu_traffic.json"
+        flop = 6.0 * cfg.D * last["loss_pairs"]                 # 3 FMA per (pair, column): a4, a6 (x2)
         out = {
             "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config],
-                       "V": cfg.V, "D": cfg.D, "n_tokens": n, "full_size": n == cfg.n, "sync_period_words": args.sync_period if world > 1 else None,
-                       "sync": (("C13 full average every interval" if hot == 0 else
-                                 f"C14: rows [0,{hot}) averaged every interval, the rest every {cold}th and at the end")
-                                + ("; C15: each average in flight during the next interval, applied one interval late"
-                                   if ovl else "")) if world > 1 else None,
-                       "parallelism": f"dp{world} corpus-sharded replicas" if world > 1 else "single GPU",
-                       "l2": f"no flush: corpus ({n_local * 4 / 1e9:.1f} GB) and model ({cfg.V * cfg.D * 8 / 1e9:.2f} GB) exceed the 126 MB L2",
-                       "units_per_sm": last["units_per_sm"], "mode": "hogwild", "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1"}.get(last["kernel"]),
-                       "algorithm": "hogbatch" if args.algorithm == "hogbatch" else "alg1 (PAPER.md:37-63, level-1 baseline)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "hogbatch_step" if args.algorithm == "hogbatch" else "alg1",
-                         "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
-                         "row_bytes_per_word": last["bytes_row"] / n_local,
-                         "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)},
-            "roofline_l2": l2roof,
-            "rowpath_roof": None if roof is None else {
-                "value": roof, "unit": "words/s", "frac": (n / (kern_max / 1e3)) / roof,
-                "how": "same step kernel, launch configuration and batch stream with a4-a6 skipped (zero "
-                       "deltas reduced): the gather/scatter path alone; frac = step-kernel words/s / roof"},
+            "config": workload_config(args, world),
+            "run": {"units_per_sm": last["units_per_sm"], "mode": "hogwild",
+                    "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1", 5: "ring"}.get(last["kernel"]),
+                    "step_launches_per_step": last["step_launches"]},
+            # per call the library reads back its setup info (32 B) before training and its
+            # statistics (72 B) + finite-check flag block (32 B) after it
             "e2e": {"value": e2e_value, "unit": "words/s", "h2d_bytes_per_step": n_local * 4,
-                    "d2h_bytes_per_step": 64},
+                    "d2h_bytes_per_step": 32 + 72 + 32, "steps": args.steps},
             "gpu_launches": int(sum(s["launches"] for s in steps)),
             "clocks": clk.summary(),
-            "stats": {"loss_per_pair": last["loss_sum"] / max(last["loss_pairs"], 1),
-                      "ms_setup": last["ms_setup"], "ms_step": last["ms_step"], "ms_sync": last["ms_sync"],
-                      "syncs": last["syncs"]},
         }
+        l2cap = caps and caps.get("l2_rowpath_gbs")
+        if l2cap:
+            out["roofline"] = {
+                "bound": "l2", "achieved": bps / 1e9, "peak": l2cap, "unit": "GB/s", "frac": bps / 1e9 / l2cap,
+                "traffic": traffic, "kernel": "hogbatch_step" if args.algorithm == "hogbatch" else "alg1",
+                "what": "algorithmic row bytes B_row = row_touches x 4D x 2 (gather + scatter) per launch / "
+                        "step-kernel time; peak = in-run cap of the same access pattern (tools/peaks.cu "
+                        f"peaks_l2_rowpath: bulk gather + bulk reduce of {4 * cfg.D}-B rows, "
+                        f"{max(1, round(rows_per_target))} rows per batch, L2-resident, all SMs)",
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
+                "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)}
+        else:  # tools lib missing: report against HBM only
+            out["roofline"] = {"bound": "hbm", "achieved": bps / 1e9, "peak": peak, "unit": "GB/s",
+                               "frac": bps / 1e9 / peak, "traffic": traffic}
+        out["roofline_hbm"] = {
+            "bound": "hbm", "achieved": bps / 1e9, "peak": peak, "unit": "GB/s", "frac": bps / 1e9 / peak,
+            "peak_source": peak_src, "row_bytes_per_word": last["bytes_row"] / n_local,
+            "what": "BASELINE.json's gather/scatter HBM roofline fraction (R_HBM, SURVEY.md §8(d)): B_row rate / "
+                    "HBM copy bandwidth; > 1 because L2 serves the Zipf-hot rows",
+            "dram_frac": None if traffic is None else traffic * max(last["step_launches"], 1) / kern_s / 1e9 / peak}
+        if caps:
+            bcold = last["row_touches_cold"] * 4 * cfg.D * 2
+            t_roof = max(last["bytes_row"] / (l2cap * 1e9) if l2cap else 0.0, bcold / (peak * 1e9),
+                         flop / (caps.get("ffma2_tflops", 1e9) * 1e12))
+            out["roofline_cache"] = {
+                "frac": t_roof / kern_s, "t_roof_ms": t_roof * 1e3, "t_meas_ms": kern_s * 1e3,
+                "b_row": last["bytes_row"], "b_cold": bcold, "cold_from_row": last["cold_from_row"],
+                "what": "T_roof = max(B_row / L2 row-path cap, B_cold / HBM, FLOP / FFMA2 peak) over the step-kernel "
+                        "time (SURVEY.md §8(d)); B_cold = touches of rows outside the L2-sized hot prefix x 4D x 2"}
+            out["fma"] = {"achieved_tflops": flop / kern_s / 1e12, "peak_tflops": caps.get("ffma2_tflops"),
+                          "frac": flop / kern_s / 1e12 / caps["ffma2_tflops"] if caps.get("ffma2_tflops") else None,
+                          "what": "6 D FLOP per (input, output) pair (a4 dots, a6 both updates) / step-kernel time vs "
+                                  "the in-run FFMA2 peak (tools/peaks.cu peaks_ffma2)"}
+            out["caps"] = caps
+        if roof is not None:
+            out["rowpath_roof"] = {
+                "value": roof, "unit": "words/s", "frac": (n / (kern_max / 1e3)) / roof,
+                "how": "same step kernel, launch configuration and batch stream with a4-a6 skipped (zero "
+                       "deltas reduced): the gather/scatter path alone; frac = step-kernel words/s / roof"}
+        out["stats"] = {"loss_per_pair": last["loss_sum"] / max(last["loss_pairs"], 1),
+                        "ms_setup": last["ms_setup"], "ms_step": last["ms_step"], "ms_batch": last["ms_batch"],
+                        "ms_sync": last["ms_sync"], "syncs": last["syncs"], "syncs_hot": last["syncs_hot"],
+                        "targets_per_word": last["targets"] / n_local, "rows_per_target": rows_per_target}
         if world == 1 and not args.no_cpu_baseline and cfg.V * cfg.D <= 300_000_000:
             out["cpu_baseline"] = cpu_baseline(cfg, BASE_SAMPLE)
         elif world == 1 and not args.no_cpu_baseline:
@@ -347,16 +444,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rowpath", action="store_true", help="skip the rowpath_only roof run")
     ap.add_argument("--kernel", type=int, default=0,
-                    help="0 auto, 1 per-target rows, 2 window-resident rows, 3 window-resident warp-specialised")
-    ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a cfg3 prefix")
+                    help="0 auto, 1 per-target rows, 2 window-resident rows, 3 window-resident warp-specialised, "
+                         "4 ring (window-resident M_in rows, originals in TMEM)")
+    ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a prefix of the config")
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=CFG,
                     help="BASELINE.json config (3 = the headline workload; 4, 5 = the larger-tile / 4M-vocab ones)")
     ap.add_argument("--sync-period", type=int, default=SYNC_P, help="words per GPU between model averagings")
-    ap.add_argument("--sync-hot-rows", type=int, default=-1,
-                    help="C14 hot prefix averaged every interval (0 = all rows, C13; -1 = V/20 when N > 1)")
-    ap.add_argument("--sync-cold-every", type=int, default=0,
-                    help="C14 cold rows averaged every this many intervals (0 = 32 when N > 1)")
+    ap.add_argument("--sync-hot-rows", type=int, default=0,
+                    help="C14 hot prefix averaged every interval (0 = all rows: C13, the default)")
+    ap.add_argument("--sync-cold-every", type=int, default=1,
+                    help="C14 cold rows averaged every this many intervals (1 = every interval: C13)")
     ap.add_argument("--sync-overlap", type=int, default=0, help="C15 overlapped averaging (1 = on)")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
                     help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")

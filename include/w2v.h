@@ -33,6 +33,8 @@ extern "C" {
 #define W2V_ECUDA  (-4)   /* CUDA runtime error                                               */
 #define W2V_ENCCL  (-5)   /* NCCL error or NCCL library not loadable                          */
 #define W2V_ENUMERIC (-6) /* the model holds NaN/Inf after w2v_train (option check_finite)     */
+#define W2V_EPEER  (-7)   /* data-parallel: another rank failed before the first model average;
+                           * every rank returns (no collective is left waiting)              */
 
 typedef struct {
     int64_t words;        /* raw corpus tokens processed (R14: the unit of words/s)           */
@@ -59,6 +61,11 @@ typedef struct {
     int64_t l2_carve_bytes;  /* a8: persisting-L2 carve-out set for the last w2v_train (0 = off) */
     int64_t syncs_hot;       /* C14 averagings of the hot-row prefix only (syncs counts full ones) */
     int64_t units_per_sm;    /* step-kernel work units (1-warp CTAs) resident per SM, last train   */
+    int64_t row_touches_cold;/* row touches (gathered rows) of the last w2v_train whose id is >=
+                                cold_from_row: outside the Zipf-hot prefix that fits the 126 MB L2
+                                (ids are frequency ranks), i.e. the rows that must come from DRAM
+                                under an ideal static cache — B_cold of SURVEY.md §8(d)           */
+    int64_t cold_from_row;   /* that prefix: L2 bytes / (8 D) rows, last train                    */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").

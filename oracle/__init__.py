@@ -19,6 +19,12 @@ _SRC = os.path.join(_HERE, "w2v_oracle.c")
 CFLAGS = ["-O2", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math"]
 
 
+# TIMING-ONLY build (bench.py's cpu_baseline / reference arm): the same source in fp32 with
+# -O3 -march=native for the host it runs on, FMA contraction allowed. Never a parity value; built
+# on the box that times it (build_native), because -march=native code may not run elsewhere.
+CFLAGS_NATIVE = ["-O3", "-march=native", "-fPIC", "-shared", "-fno-fast-math"]
+
+
 def _so(prec: str) -> str:
     return os.path.join(_HERE, f"liboracle_{prec}.so")
 
@@ -28,6 +34,13 @@ def build(force: bool = False) -> None:
         so = _so(prec)
         if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
             subprocess.check_call(["gcc", *CFLAGS, f"-DREAL={real}", _SRC, "-o", so, "-lm", "-pthread"])
+
+
+def build_native() -> str:
+    """(Re)build the timing-only fp32 -O3 -march=native oracle for THIS host; returns its flags."""
+    subprocess.check_call(["gcc", *CFLAGS_NATIVE, "-DREAL=float", _SRC, "-o", _so("f32native"), "-lm", "-pthread"])
+    _libs.pop("f32native", None)
+    return " ".join(CFLAGS_NATIVE) + " -DREAL=float"
 
 
 class OrcParams(ctypes.Structure):
@@ -65,7 +78,11 @@ def _p(a, t):
 
 def lib(prec: str = "f64"):
     if prec not in _libs:
-        build()
+        if prec == "f32native":
+            if not os.path.exists(_so(prec)):
+                build_native()
+        else:
+            build()
         L = ctypes.CDLL(_so(prec))
         u32p, u64p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)
         i32p, i64p = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)
@@ -109,7 +126,7 @@ def lib(prec: str = "f64"):
 
 
 def real_dtype(prec: str):
-    return np.float64 if prec == "f64" else np.float32
+    return np.float64 if prec == "f64" else np.float32   # "f32" and the timing-only "f32native"
 
 
 # ------------------------------------------------------------------ primitives ---------------

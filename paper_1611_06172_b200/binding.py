@@ -17,7 +17,7 @@ if not os.path.exists(_SO):
     raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
 _lib = ctypes.CDLL(_SO)
 
-OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENUMERIC = 0, -1, -2, -3, -4, -5, -6
+OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENUMERIC, EPEER = 0, -1, -2, -3, -4, -5, -6, -7
 
 
 class Stats(ctypes.Structure):
@@ -28,7 +28,8 @@ class Stats(ctypes.Structure):
                 ("step_launches", ctypes.c_int64), ("bytes_row", ctypes.c_int64),
                 ("loss_tail_sum", ctypes.c_double), ("loss_tail_pairs", ctypes.c_int64), ("kernel", ctypes.c_int64),
                 ("ms_batch", ctypes.c_double), ("l2_window_bytes", ctypes.c_int64), ("l2_carve_bytes", ctypes.c_int64),
-                ("syncs_hot", ctypes.c_int64), ("units_per_sm", ctypes.c_int64)]
+                ("syncs_hot", ctypes.c_int64), ("units_per_sm", ctypes.c_int64),
+                ("row_touches_cold", ctypes.c_int64), ("cold_from_row", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -67,14 +68,39 @@ def _check(rc):
     return rc
 
 
+_dims = {}   # V, D, window, K of the live context (set by init): argument checks only
+
+
 def _ptr(a):
     if a is None:
         return None
     if hasattr(a, "data_ptr"):          # torch.Tensor (host or device)
-        assert a.is_contiguous()
+        if not a.is_contiguous():
+            raise ValueError("array must be contiguous")
         return a.data_ptr()
-    assert isinstance(a, np.ndarray) and a.flags.c_contiguous
+    if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+        raise ValueError("array must be a C-contiguous numpy array or a contiguous torch tensor")
     return a.ctypes.data
+
+
+def _dtype_name(a) -> str:
+    return str(a.dtype).replace("torch.", "")
+
+
+def _numel(a) -> int:
+    return int(a.numel()) if hasattr(a, "numel") else int(a.size)
+
+
+def _checked(a, dtype: str, need: int, what: str):
+    """Pointer of `a` after checking its element type and that it holds >= `need` elements: the
+    library sees only a pointer, so an int64 corpus or a short buffer would be misread."""
+    if a is None:
+        raise ValueError(f"{what}: array is None")
+    if _dtype_name(a) != dtype:
+        raise TypeError(f"{what}: dtype {_dtype_name(a)}, expected {dtype}")
+    if _numel(a) < need:
+        raise ValueError(f"{what}: {_numel(a)} elements, need >= {need}")
+    return _ptr(a)
 
 
 def library_path() -> str:
@@ -82,7 +108,9 @@ def library_path() -> str:
 
 
 def init(V, D, window, K, alpha, subsample, seed):
-    return _check(_lib.w2v_init(V, D, window, K, alpha, subsample, seed))
+    rc = _check(_lib.w2v_init(V, D, window, K, alpha, subsample, seed))
+    _dims.update(V=int(V), D=int(D), window=int(window), K=int(K))
+    return rc
 
 
 def set_option(key: str, value: int):
@@ -94,20 +122,24 @@ def set_stream(stream_handle):
 
 
 def train(corpus_ids, n_tokens=None, epochs=1):
-    n = int(corpus_ids.numel() if hasattr(corpus_ids, "numel") else corpus_ids.size) if n_tokens is None else n_tokens
-    return _check(_lib.w2v_train(_ptr(corpus_ids), n, epochs))
+    n = _numel(corpus_ids) if n_tokens is None else int(n_tokens)
+    return _check(_lib.w2v_train(_checked(corpus_ids, "int32", n, "train corpus_ids"), n, epochs))
 
 
 def sync():
     return _check(_lib.w2v_sync())
 
 
+def _model_elems() -> int:
+    return _dims.get("V", 0) * _dims.get("D", 0)
+
+
 def get_embeddings(which, dst):
-    return _check(_lib.w2v_get_embeddings(which, _ptr(dst)))
+    return _check(_lib.w2v_get_embeddings(which, _checked(dst, "float32", _model_elems(), "get_embeddings dst")))
 
 
 def set_embeddings(which, src):
-    return _check(_lib.w2v_set_embeddings(which, _ptr(src)))
+    return _check(_lib.w2v_set_embeddings(which, _checked(src, "float32", _model_elems(), "set_embeddings src")))
 
 
 def get_stats() -> dict:
@@ -117,10 +149,19 @@ def get_stats() -> dict:
 
 
 def debug_batches(keep=None, b=None, N=None, ctx=None, neg=None):
-    return _check(_lib.w2v_debug_batches(_ptr(keep), _ptr(b), _ptr(N), _ptr(ctx), _ptr(neg)))
+    """Buffers sized for the recorded window (option debug_len): u8 keep/b/N [len], int32
+    ctx [len][2*window], int32 neg [len][max(K,1)]; any may be None."""
+    def chk(a, dt, what):
+        if a is not None and _dtype_name(a) != dt:
+            raise TypeError(f"debug_batches {what}: dtype {_dtype_name(a)}, expected {dt}")
+        return _ptr(a)
+    return _check(_lib.w2v_debug_batches(chk(keep, "uint8", "keep"), chk(b, "uint8", "b"), chk(N, "uint8", "N"),
+                                         chk(ctx, "int32", "ctx"), chk(neg, "int32", "neg")))
 
 
 def debug_alg1_negatives(neg):
+    if _dtype_name(neg) != "int32":
+        raise TypeError("debug_alg1_negatives: int32 buffer expected")
     return _check(_lib.w2v_debug_alg1_negatives(_ptr(neg)))
 
 
@@ -152,4 +193,5 @@ def dist_shard(n_global, L, world, rank):
 
 
 def finalize():
+    _dims.clear()
     return _check(_lib.w2v_finalize())

@@ -87,7 +87,7 @@ struct Ctx {
     int64_t sync_hot_rows = 0;   // C14: hot prefix averaged every interval (0 = all rows)
     int64_t sync_cold_every = 1; // C14: the other rows every this many intervals (and the last)
     int sync_overlap = 0;        // C15: average in flight during the next interval (one late)
-    float *syS = nullptr, *syC = nullptr;  // C15 snapshot (averaged in place) and its copy
+    float *syS = nullptr, *syC = nullptr;  // C15: average (S) of the snapshot (C), out of place
     cudaStream_t comm_stream = nullptr;
     int64_t Q = 10000;
     int allow_tn = 0;
@@ -225,6 +225,25 @@ struct EventPool {
     }
 };
 
+// a8 option l2_persist: the persisting-L2 carve-out and the stream's access-policy window are
+// process-wide state; undo both (window off, persisting lines reset, previous limit) on every
+// exit path of w2v_train so later calls and other work get the whole L2 back.
+struct L2WindowGuard {
+    bool window_set = false, limit_set = false;
+    size_t prev_limit = 0;
+    cudaStream_t stream = nullptr;
+    ~L2WindowGuard() {
+        if (window_set) {
+            cudaStreamAttrValue a{};
+            a.accessPolicyWindow.num_bytes = 0;
+            cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &a);
+            cudaCtxResetPersistingL2Cache();
+        }
+        if (limit_set) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev_limit);
+        cudaGetLastError();
+    }
+};
+
 // C13 host plan
 struct Plan {
     int64_t S, lo, hi, start, end, J, I;
@@ -264,6 +283,24 @@ int sync_models(int64_t row_lo = 0, int64_t row_hi = -1) {
         NC(g_nccl.commGetAsyncError(g.comm, &ae));
         NC(ae);
     }
+    return W2V_OK;
+}
+
+// Data-parallel error consensus: every rank passes its local status; if any rank failed, all
+// ranks return (the failing ones their own error, the others W2V_EPEER) instead of leaving peers
+// blocked in the next collective (DESIGN.md §2 C13). No-op without a communicator.
+int dp_agree(int rc_local, cudaStream_t st) {
+    if (!dp()) return rc_local;
+    const std::string own = g_err;
+    std::vector<int64_t> h(g.world, 0);
+    h[g.rank] = rc_local != 0 ? 1 : 0;
+    CU(cudaMemcpyAsync(g.dp_tmp, h.data(), (size_t)g.world * 8, cudaMemcpyHostToDevice, st));
+    NC(g_nccl.allReduce(g.dp_tmp, g.dp_tmp, (size_t)g.world, ncclInt64, ncclSum, g.comm, st));
+    CU(cudaMemcpyAsync(h.data(), g.dp_tmp, (size_t)g.world * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (rc_local != 0) { g_err = own; return rc_local; }
+    for (int q = 0; q < g.world; ++q)
+        if (h[q]) return fail(W2V_EPEER, "w2v_train: rank %d failed during setup; nothing trained on any rank", q);
     return W2V_OK;
 }
 
@@ -394,6 +431,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaEventRecord(ev_h2d, st));
     // ---- a0: shard geometry (C13), counts, thresholds, sampler
     int64_t n_global = n, shard_start = 0;
+    bool bad_shard = false;
     if (dp()) {
         if (!g.dp_tmp) { int rc = dmalloc((void**)&g.dp_tmp, (size_t)g.world * 8, "dp scratch"); if (rc) return rc; }
         std::vector<int64_t> h(g.world, 0);
@@ -406,10 +444,14 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         for (int q = 0; q < g.world; ++q) { if (q < g.rank) shard_start += h[q]; n_global += h[q]; }
         if (n_global == 0) return W2V_OK;
         const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
-        if (pl.start != shard_start || pl.end - pl.start != n)
-            return fail(W2V_EINVAL, "w2v_train: rank %d shard [%lld,%lld) is not the C13 shard [%lld,%lld) of n=%lld, L=%d",
-                        g.rank, (long long)shard_start, (long long)(shard_start + n), (long long)pl.start,
-                        (long long)pl.end, (long long)n_global, g.L);
+        if (pl.start != shard_start || pl.end - pl.start != n) {
+            // rank-local error: reported after the setup collectives below, which every rank
+            // still joins, so no peer is left blocked
+            bad_shard = true;
+            fail(W2V_EINVAL, "w2v_train: rank %d shard [%lld,%lld) is not the C13 shard [%lld,%lld) of n=%lld, L=%d",
+                 g.rank, (long long)shard_start, (long long)(shard_start + n), (long long)pl.start,
+                 (long long)pl.end, (long long)n_global, g.L);
+        }
     }
     CU(cudaMemsetAsync(g.counts, 0, (size_t)g.V * 8, st));
     CU(cudaMemsetAsync(g.info, 0, sizeof(SetupInfo), st));
@@ -420,41 +462,56 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaMemcpyAsync(&hinfo, g.info, sizeof hinfo, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (dp()) {
-        // every rank must take the same exit: combine the bad-id flags
+        // every rank must take the same exit: combine the bad-id and bad-shard flags
         std::vector<int64_t> h(g.world, 0);
-        h[g.rank] = hinfo.bad_id;
+        h[g.rank] = hinfo.bad_id | (bad_shard ? 2 : 0);
         CU(cudaMemcpyAsync(g.dp_tmp, h.data(), (size_t)g.world * 8, cudaMemcpyHostToDevice, st));
         NC(g_nccl.allReduce(g.dp_tmp, g.dp_tmp, (size_t)g.world, ncclInt64, ncclSum, g.comm, st));
         CU(cudaMemcpyAsync(h.data(), g.dp_tmp, (size_t)g.world * 8, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
-        for (int q = 0; q < g.world; ++q) hinfo.bad_id |= (int)h[q];
+        if (bad_shard) return W2V_EINVAL;  // message set above
+        for (int q = 0; q < g.world; ++q) {
+            hinfo.bad_id |= (int)(h[q] & 1);
+            if (h[q] & 2) return fail(W2V_EPEER, "w2v_train: rank %d passed a shard that is not its C13 shard", q);
+        }
     }
     if (hinfo.bad_id) return fail(W2V_EINVAL, "w2v_train: corpus contains an id outside [0,%lld); nothing trained", (long long)g.V);
     if (hinfo.PV == 0) return fail(W2V_EINVAL, "w2v_train: sampler mass P[V] is 0");
     CU(cudaEventRecord(ev_setup, st));
+    // Everything from here to the first step launch may fail on one rank only (allocation,
+    // occupancy): with a communicator, every exit of this region goes through one consensus
+    // collective (dp_agree), so a failing rank never leaves its peers blocked in an all-reduce.
+    auto bail = [&](int rc) -> int { return dp() ? dp_agree(rc, st) : rc; };
+#define CUB(expr)                                                                                 \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess) return bail(fail(W2V_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_))); \
+    } while (0)
     // ---- debug buffers
     free_dbg();
     if (g.dbg_len > 0) {
         const int64_t Lq = g.dbg_len, kk = g.K > 0 ? g.K : 1;
         int rc;
-        if ((rc = dmalloc((void**)&g.dbg_keep, Lq, "debug keep"))) return rc;
-        if ((rc = dmalloc((void**)&g.dbg_b, Lq, "debug b"))) return rc;
-        if ((rc = dmalloc((void**)&g.dbg_N, Lq, "debug N"))) return rc;
-        if ((rc = dmalloc((void**)&g.dbg_ctx, (size_t)Lq * 2 * g.window * 4, "debug ctx"))) return rc;
-        if ((rc = dmalloc((void**)&g.dbg_neg, (size_t)Lq * kk * 4, "debug neg"))) return rc;
-        CU(cudaMemsetAsync(g.dbg_keep, 0, Lq, st));
-        CU(cudaMemsetAsync(g.dbg_b, 0, Lq, st));
-        CU(cudaMemsetAsync(g.dbg_N, 0, Lq, st));
-        CU(cudaMemsetAsync(g.dbg_ctx, 0xff, (size_t)Lq * 2 * g.window * 4, st));
-        CU(cudaMemsetAsync(g.dbg_neg, 0xff, (size_t)Lq * kk * 4, st));
+        if ((rc = dmalloc((void**)&g.dbg_keep, Lq, "debug keep"))) return bail(rc);
+        if ((rc = dmalloc((void**)&g.dbg_b, Lq, "debug b"))) return bail(rc);
+        if ((rc = dmalloc((void**)&g.dbg_N, Lq, "debug N"))) return bail(rc);
+        if ((rc = dmalloc((void**)&g.dbg_ctx, (size_t)Lq * 2 * g.window * 4, "debug ctx"))) return bail(rc);
+        if ((rc = dmalloc((void**)&g.dbg_neg, (size_t)Lq * kk * 4, "debug neg"))) return bail(rc);
+        CUB(cudaMemsetAsync(g.dbg_keep, 0, Lq, st));
+        CUB(cudaMemsetAsync(g.dbg_b, 0, Lq, st));
+        CUB(cudaMemsetAsync(g.dbg_N, 0, Lq, st));
+        CUB(cudaMemsetAsync(g.dbg_ctx, 0xff, (size_t)Lq * 2 * g.window * 4, st));
+        CUB(cudaMemsetAsync(g.dbg_neg, 0xff, (size_t)Lq * kk * 4, st));
         if (g.algorithm == 1) {
-            if ((rc = dmalloc((void**)&g.dbg_a1neg, (size_t)Lq * 2 * g.window * kk * 4, "debug Alg.1 negatives"))) return rc;
-            CU(cudaMemsetAsync(g.dbg_a1neg, 0xff, (size_t)Lq * 2 * g.window * kk * 4, st));
+            if ((rc = dmalloc((void**)&g.dbg_a1neg, (size_t)Lq * 2 * g.window * kk * 4, "debug Alg.1 negatives"))) return bail(rc);
+            CUB(cudaMemsetAsync(g.dbg_a1neg, 0xff, (size_t)Lq * 2 * g.window * kk * 4, st));
         }
         g.dbg_rec_len = Lq;
     }
-    // ---- a8: persisting-L2 window over the hot prefix rows of [M_in|M_out]
-    bool window_set = false;
+    // ---- a8: persisting-L2 window over the hot prefix rows of [M_in|M_out] (option; measured
+    // harmful). The carve-out limit and the stream window are restored on every exit path.
+    L2WindowGuard l2guard;
+    bool& window_set = l2guard.window_set;
     g.st.l2_window_bytes = g.st.l2_carve_bytes = 0;
     if (g.l2_persist && g.mode == 0) {
         int maxp = 0, maxwin = 0;
@@ -466,7 +523,12 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
             size_t bytes = g.l2_window_rows > 0 ? (size_t)g.l2_window_rows * rowb : carve;
             bytes = std::min<size_t>(bytes, (size_t)maxwin);
             bytes = std::min<size_t>(bytes, (size_t)g.V * rowb);
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+            size_t prev = 0;
+            if (cudaDeviceGetLimit(&prev, cudaLimitPersistingL2CacheSize) == cudaSuccess &&
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+                l2guard.limit_set = true;
+                l2guard.prev_limit = prev;
+                l2guard.stream = st;
                 cudaStreamAttrValue a{};
                 a.accessPolicyWindow.base_ptr = g.M;
                 a.accessPolicyWindow.num_bytes = bytes;
@@ -506,10 +568,16 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.dbg_a1neg = g.dbg_a1neg;
     p.algorithm = g.algorithm;
     p.rowpath_only = g.rowpath_only;
+    {   // cache-aware roofline statistics: the hot prefix whose half-rows of both matrices fill L2
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g.device);
+        p.cold_from = (int64_t)l2 / ((int64_t)8 * g.D);
+        g.st.cold_from_row = p.cold_from;
+    }
     if (g.rowpath_only && (g.algorithm != 0 || (g.kernel != 0 && g.kernel != 1)))
-        return fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows kernel (kernel 0/1, algorithm 0)");
+        return bail(fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows kernel (kernel 0/1, algorithm 0)"));
     if (g.algorithm == 1 && !alg1_supported(g.D, g.K))
-        return fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K);
+        return bail(fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K));
     // kernel choice: 1 per-target rows, 2 window-resident (one warp per unit),
     // 3 window-resident warp-specialised (a CTA of column warps + an IO warp per unit)
     int32_t off_win = 0, off_row = 0, off_wg = 0;
@@ -520,26 +588,26 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     int kern = g.kernel == 0 ? 1 : g.kernel;
     if (g.algorithm == 1) kern = 0;  // alg1.cu
     if (kern == 2 && !(wb_win > 0 && wb_win <= kSmemMax))
-        return fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
+        return bail(fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L));
     if (kern == 3 && !(wb_wg > 0 && wb_wg <= kSmemMax))
-        return fail(W2V_EINVAL, "w2v_train: kernel=3 (window, warp-specialised) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L);
+        return bail(fail(W2V_EINVAL, "w2v_train: kernel=3 (window, warp-specialised) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L));
     const bool use_win = kern == 2;
     size_t wb = kern == 3 ? wb_wg : use_win ? wb_win : wb_row;
     if (kern == 0) wb = alg1_warp_bytes(g.L);
     p.slab_offset = kern == 3 ? off_wg : use_win ? off_win : off_row;
-    if (wb == 0 || wb > kSmemMax) return fail(W2V_EINVAL, "w2v_train: shared memory per work unit %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb);
+    if (wb == 0 || wb > kSmemMax) return bail(fail(W2V_EINVAL, "w2v_train: shared memory per work unit %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb));
     p.warp_bytes = (int32_t)wb;
     int ctas = 1;
     if (g.mode == 0) {
         int occ = kern == 0 ? alg1_max_ctas_per_sm(p) : kern == 3 ? wg_max_ctas_per_sm(p)
                 : use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
-        if (occ < 1) return fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per work unit)", wb);
+        if (occ < 1) return bail(fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per work unit)", wb));
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
     g.st.units_per_sm = ctas >= g.sms ? ctas / g.sms : 1;
     g.st.kernel = kern == 0 ? 4 : kern;  // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1
-    CU(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
+    CUB(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
     const int64_t chunk_hi = (shard_start + n + g.L - 1) / g.L;
@@ -555,7 +623,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     {
         int rc = ensure_bt(std::min<int64_t>(per, std::max<int64_t>(chunk_hi - chunk_lo, 1)), p.Lp, negs_per_slot,
                            g.overlap_batch ? 2 : 1);
-        if (rc) return rc;
+        if (rc) return bail(rc);
     }
     p.bt_redo = g.bt_redo;
     auto use_set = [&](StepParams& q, int set) {
@@ -565,28 +633,33 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     // runs on the main one (the step kernel's slabs leave room for one batch block per SM)
     const bool ovl = g.overlap_batch != 0;
     cudaEvent_t ev_tables, ev_bdone[2], ev_sdone[2];
-    CU(pool.make(&ev_tables, cudaEventDisableTiming));
+    CUB(pool.make(&ev_tables, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
-        CU(pool.make(&ev_bdone[i], cudaEventDisableTiming));
-        CU(pool.make(&ev_sdone[i], cudaEventDisableTiming));
+        CUB(pool.make(&ev_bdone[i], cudaEventDisableTiming));
+        CUB(pool.make(&ev_sdone[i], cudaEventDisableTiming));
     }
-    CU(cudaEventRecord(ev_tables, st));
+    CUB(cudaEventRecord(ev_tables, st));
     if (ovl) {
-        CU(cudaStreamWaitEvent(g.side, ev_tables, 0));
-        for (int i = 0; i < 2; ++i) CU(cudaEventRecord(ev_sdone[i], st));
+        CUB(cudaStreamWaitEvent(g.side, ev_tables, 0));
+        for (int i = 0; i < 2; ++i) CUB(cudaEventRecord(ev_sdone[i], st));
     }
     std::vector<cudaEvent_t> bev;  // (start, end) pairs of the batch launches on the side stream
     // C15 state: rows [0, pend_hi) of the model have an average in flight on the comm stream
     cudaEvent_t ev_snap, ev_ar;
-    CU(pool.make(&ev_snap, cudaEventDisableTiming));
-    CU(pool.make(&ev_ar, cudaEventDisableTiming));
+    CUB(pool.make(&ev_snap, cudaEventDisableTiming));
+    CUB(pool.make(&ev_ar, cudaEventDisableTiming));
     int64_t pend_hi = 0;
     if (dp() && g.sync_overlap && !g.syS) {
         const size_t bytes = (size_t)g.V * 2 * g.Ds * sizeof(float);
         int rc;
-        if ((rc = dmalloc((void**)&g.syS, bytes, "C15 snapshot"))) return rc;
-        if ((rc = dmalloc((void**)&g.syC, bytes, "C15 snapshot copy"))) return rc;
+        if ((rc = dmalloc((void**)&g.syS, bytes, "C15 average"))) return bail(rc);
+        if ((rc = dmalloc((void**)&g.syC, bytes, "C15 snapshot"))) return bail(rc);
     }
+    {
+        const int rc = bail(W2V_OK);  // every rank reached the training loop
+        if (rc) return rc;
+    }
+#undef CUB
     int64_t jl = 0;                // launch counter (buffer set = jl & 1)
     std::vector<cudaEvent_t> evs;
     std::vector<int> ev_kind;  // 0 step, 1 sync, 2 batch
@@ -654,10 +727,11 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                         if (rc) return rc;
                     } else {
                         const int64_t hi_r = full ? g.V : H;
-                        CU(launch_sync_snap(g.M, g.syS, g.syC, (size_t)hi_r * rowf, g.sms, st));
+                        // snapshot C = M[rows]; out-of-place average C -> S in flight
+                        CU(launch_sync_snap(g.M, g.syC, (size_t)hi_r * rowf, g.sms, st));
                         CU(cudaEventRecord(ev_snap, st));
                         CU(cudaStreamWaitEvent(g.comm_stream, ev_snap, 0));
-                        NC(g_nccl.allReduce(g.syS, g.syS, (size_t)hi_r * rowf, ncclFloat32, ncclAvg, g.comm,
+                        NC(g_nccl.allReduce(g.syC, g.syS, (size_t)hi_r * rowf, ncclFloat32, ncclAvg, g.comm,
                                             g.comm_stream));
                         CU(cudaEventRecord(ev_ar, g.comm_stream));
                         pend_hi = hi_r;
@@ -681,13 +755,6 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     step_phase_report();
     win_phase_report();
     wg_phase_report();
-    if (window_set) {
-        cudaStreamAttrValue a{};
-        a.accessPolicyWindow.num_bytes = 0;
-        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
-        cudaCtxResetPersistingL2Cache();
-        cudaGetLastError();
-    }
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, ev0, ev_end)); g.st.ms_total = ms;
     CU(cudaEventElapsedTime(&ms, ev0, ev_h2d)); g.st.ms_h2d = ms;
@@ -712,6 +779,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     g.st.loss_tail_pairs += (int64_t)hs.loss_tail_pairs;
     g.st.launches = launches;
     g.st.bytes_row = (int64_t)hs.row_touches * 4 * g.D * 2;
+    g.st.row_touches_cold = (int64_t)hs.row_touches_cold;
     if (g.check_finite && hend.nonfinite)
         return fail(W2V_ENUMERIC, "w2v_train: the model holds NaN/Inf after training (diverged; lower alpha)");
     return W2V_OK;
@@ -795,6 +863,21 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);
     NC(g_nccl.commInitRank(&g.comm, world, uid, rank));
+    if (world > 1 && g.Ds != g.D) {
+        // every model average moves 2*V*Ds floats: drop the 128-B row padding (worth ~0.7% on
+        // one GPU) so the all-reduce sends exactly the 2*V*D model floats
+        float* M2 = nullptr;
+        int rc = dmalloc((void**)&M2, (size_t)g.V * 2 * g.D * sizeof(float), "the unpadded data-parallel model");
+        if (rc) return rc;
+        const size_t half = (size_t)g.D * 4;
+        for (int h = 0; h < 2; ++h)
+            CU(cudaMemcpy2DAsync(M2 + h * g.D, 2 * half, g.M + h * g.Ds, (size_t)2 * g.Ds * 4, half, (size_t)g.V,
+                                 cudaMemcpyDeviceToDevice, g.stream));
+        CU(cudaStreamSynchronize(g.stream));
+        cudaFree(g.M);
+        g.M = M2;
+        g.Ds = g.D;
+    }
     return W2V_OK;
 }
 

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
     W2V_T(unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0, st_tail_pairs = 0;
+    unsigned st_cold = 0;  // this lane's gathered rows with id >= cold_from
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
 
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             __syncwarp();
             for (int r = lane; r < R; r += 32) {
                 const int32_t id = rowid[r];
+                st_cold += id >= p.cold_from;
                 float* dst = r < N ? As + r * RS : Bs + (r - N) * RS;
 #ifndef W2V_ABL_NOGATHER
                 bulk_g2s_hint(dst, p.M + (size_t)id * 2 * Ds + (r < N ? 0 : Ds), rowbytes, mbar,
@@ -356,6 +358,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     for (int o = 16; o > 0; o >>= 1) {
         st_loss += __shfl_xor_sync(kFull, st_loss, o);
         st_tail += __shfl_xor_sync(kFull, st_tail, o);
+        st_cold += __shfl_xor_sync(kFull, st_cold, o);
     }
     W2V_T(if (lane == 0) for (int i = 0; i < 8; ++i) atomicAdd(&g_phase[i], ph[i]);)
     if (lane == 0) {
@@ -364,6 +367,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         atomicAdd(&p.stats->row_touches, st_touch);
         atomicAdd(&p.stats->loss_pairs, st_pairs);
         atomicAdd(&p.stats->loss_sum, st_loss);
+        atomicAdd(&p.stats->row_touches_cold, (unsigned long long)st_cold);
         if (st_tail_pairs) {
             atomicAdd(&p.stats->loss_tail_sum, st_tail);
             atomicAdd(&p.stats->loss_tail_pairs, st_tail_pairs);

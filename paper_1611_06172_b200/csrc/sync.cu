@@ -1,7 +1,7 @@
 // sync.cu — C15: the element-wise halves of the overlapped model average (a9,
-// SURVEY.md §8(f) NEXT-2). After interval k the rows due are snapshot (S = C = M) and S is
-// averaged by NCCL on the comm stream while interval k+1 trains; after interval k+1 the replica
-// applies the average's correction M += S - C. Both passes are HBM-bound streams over the
+// SURVEY.md §8(f) NEXT-2). After interval k the rows due are snapshot (C = M) and averaged by an
+// OUT-OF-PLACE NCCL all-reduce (C -> S) on the comm stream while interval k+1 trains; after
+// interval k+1 the replica applies the average's correction M += S - C. Both passes are HBM-bound streams over the
 // contiguous row range of the interleaved model (float4, grid-stride, sized to the SM count).
 #include "w2v_internal.h"
 
@@ -22,12 +22,9 @@ __global__ void apply_kernel(float4* __restrict__ M, const float4* __restrict__ 
     }
 }
 
-__global__ void snap_kernel(const float4* __restrict__ M, float4* __restrict__ S, float4* __restrict__ C, size_t n4) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
-        const float4 m = M[i];
-        S[i] = m;
-        C[i] = m;
-    }
+__global__ void snap_kernel(const float4* __restrict__ M, float4* __restrict__ C, size_t n4) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+        C[i] = M[i];
 }
 
 int grid(size_t n4, int sms) {
@@ -46,11 +43,11 @@ cudaError_t launch_sync_apply(float* M, const float* S, const float* C, size_t n
     return cudaGetLastError();
 }
 
-// S[i] = C[i] = M[i] over n floats
-cudaError_t launch_sync_snap(const float* M, float* S, float* C, size_t n, int sms, cudaStream_t st) {
+// C[i] = M[i] over n floats
+cudaError_t launch_sync_snap(const float* M, float* C, size_t n, int sms, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    snap_kernel<<<grid(n / 4, sms), 256, 0, st>>>(reinterpret_cast<const float4*>(M), reinterpret_cast<float4*>(S),
-                                                  reinterpret_cast<float4*>(C), n / 4);
+    snap_kernel<<<grid(n / 4, sms), 256, 0, st>>>(reinterpret_cast<const float4*>(M), reinterpret_cast<float4*>(C),
+                                                  n / 4);
     return cudaGetLastError();
 }
 

@@ -19,6 +19,7 @@ struct DevStats {
     double loss_sum;
     double loss_tail_sum;
     unsigned long long loss_tail_pairs;
+    unsigned long long row_touches_cold;  // row touches with id >= StepParams::cold_from
 };
 
 struct StepParams {
@@ -60,6 +61,8 @@ struct StepParams {
     int64_t hot_rows_in;  // M_in rows (contexts) in the rows kernel
     int32_t l2_hint;
     int32_t rowpath_only; // measurement mode: rows kernel without a4-a6 (zero deltas; model unchanged)
+    int64_t cold_from;    // statistics: row touches with id >= cold_from are counted as "cold" (the
+                          // ids beyond an L2-sized hot prefix; the cache-aware roofline's B_cold)
     int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)
     int32_t* dbg_a1neg;   // Alg.1 debug: [len][2*window][K] per-input negatives
 };
@@ -92,7 +95,7 @@ void wg_phase_report();  // (experiment builds with W2V_PHASE_TIMING)
 
 // sync.cu (C15 overlapped averaging)
 cudaError_t launch_sync_apply(float* M, const float* S, const float* C, size_t n, int sms, cudaStream_t st);
-cudaError_t launch_sync_snap(const float* M, float* S, float* C, size_t n, int sms, cudaStream_t st);
+cudaError_t launch_sync_snap(const float* M, float* C, size_t n, int sms, cudaStream_t st);
 
 // alg1.cu (Algorithm 1, the level-1 baseline)
 bool alg1_supported(int D, int K);

@@ -22,6 +22,13 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"].startswith("cfg3")
+    # the reference arm reports the SAME workload config as the GPU arm (same metric and config)
+    sys.path.insert(0, ROOT)
+    import bench
+    args = bench.argparse.Namespace(config=3, tokens=0, sync_hot_rows=0, sync_cold_every=1, sync_overlap=0,
+                                    sync_period=bench.SYNC_P, algorithm="hogbatch")
+    assert d["config"] == json.loads(json.dumps(bench.workload_config(args, 1)))
+    assert d["dtype"] == "f32" and "cpu_model" in d["cpu_baseline"]
 
 
 def test_reference_arm_nonzero_rank_exits_quietly():

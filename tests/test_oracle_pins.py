@@ -515,3 +515,23 @@ def test_threaded_hogwild_oracle_mode_counts():
     for k in ("words", "targets", "row_touches", "loss_pairs"):
         assert res[4][2][k] == res[0][2][k], k
     assert abs(res[4][2]["loss_sum"] / res[0][2]["loss_sum"] - 1) < 0.02
+
+
+def test_counts_equal_bincount_and_reject_out_of_range():
+    """a0 histogram (SPEC.md:49-57 word counts): orc_counts equals numpy's
+    bincount exactly on Zipf, uniform and edge corpora (ids at 0 and V-1, V=1, empty corpus), and
+    an id outside [0, V) — either side — is rejected (SPEC.md:253 precondition)."""
+    rng = np.random.default_rng(11)
+    cases = [(inputs.Corpus("iid", 1000, 1.0, 3).tokens(0, 50_000), 1000),
+             (rng.integers(0, 77, 9_999).astype(np.int32), 77),
+             (np.array([0, 4, 4, 0, 4], np.int32), 5),
+             (np.zeros(17, np.int32), 1),
+             (np.zeros(0, np.int32), 3)]
+    for ids, V in cases:
+        c = oracle.counts(ids, V)
+        assert c.dtype == np.int64 and c.shape == (V,)
+        assert np.array_equal(c, np.bincount(ids, minlength=V).astype(np.int64))
+        assert int(c.sum()) == ids.size
+    for bad in (np.array([1, 2, 5], np.int32), np.array([0, -1], np.int32)):
+        with pytest.raises(ValueError):
+            oracle.counts(bad, 5)
