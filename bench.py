@@ -314,6 +314,7 @@ def run_ours(args):
     barrier()
     steps = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    before = w2v.get_stats()
     with Clocks(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
@@ -321,6 +322,10 @@ def run_ours(args):
             steps.append(w2v.get_stats())
         e1.record(stream)
         barrier()
+    # counters (words, targets, row_touches, loss_pairs, loss_sum) are cumulative since w2v_init:
+    # the last timed call's own values are differences
+    prev = steps[-2] if len(steps) > 1 else before
+    call = {k: steps[-1][k] - prev[k] for k in ("words", "targets", "row_touches", "loss_pairs", "loss_sum")}
     ms = e0.elapsed_time(e1)
     ms_step_kernel = sum(s["ms_step"] for s in steps) / len(steps)
     ms_max, kern_max = maxr(ms, ms_step_kernel)
@@ -355,7 +360,7 @@ def run_ours(args):
         peak, peak_src = peaks()
         kern_s = last["ms_step"] / 1e3
         bps = last["bytes_row"] / kern_s                       # algorithmic row bytes / s
-        rows_per_target = last["row_touches"] / max(last["targets"], 1)
+        rows_per_target = call["row_touches"] / max(call["targets"], 1)
         caps = measure_caps(4 * cfg.D, max(1, round(rows_per_target)), last["units_per_sm"])
         traffic = None   # DRAM bytes per launch (ncu --set full capture, profiles/), scaled to this launch size
         traffic_src = None
@@ -365,7 +370,7 @@ def run_ours(args):
             if tr.get("config", 3) == args.config and tr.get("kernel_id", last["kernel"]) == last["kernel"]:
                 traffic = tr.get("dram_bytes_per_word") * n_local / max(last["step_launches"], 1)
                 traffic_src = f"ncu --set full capture {tr.get('source')} ({tr.get('round')}), profiles/ncu_traffic.json"
-        flop = 6.0 * cfg.D * last["loss_pairs"]                 # 3 FMA per (pair, column): a4, a6 (x2)
+        flop = 6.0 * cfg.D * call["loss_pairs"]                 # 3 FMA per (pair, column): a4, a6 (x2)
         out = {
             "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -391,6 +396,10 @@ def run_ours(args):
                         f"peaks_l2_rowpath: bulk gather + bulk reduce of {4 * cfg.D}-B rows, "
                         f"{max(1, round(rows_per_target))} rows per batch, L2-resident, all SMs)",
                 "traffic_source": traffic_src,
+                # bytes the kernel really moved through L2 (fewer than B_row for the ring kernel,
+                # which keeps a chunk's M_in window on chip) and that rate against the same cap
+                "moved_gbs": last["bytes_moved"] / kern_s / 1e9,
+                "moved_frac": last["bytes_moved"] / kern_s / 1e9 / l2cap,
                 "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
                 "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)}
         else:  # tools lib missing: report against HBM only
@@ -421,10 +430,11 @@ def run_ours(args):
                 "value": roof, "unit": "words/s", "frac": (n / (kern_max / 1e3)) / roof,
                 "how": "same step kernel, launch configuration and batch stream with a4-a6 skipped (zero "
                        "deltas reduced): the gather/scatter path alone; frac = step-kernel words/s / roof"}
-        out["stats"] = {"loss_per_pair": last["loss_sum"] / max(last["loss_pairs"], 1),
+        out["stats"] = {"loss_per_pair": call["loss_sum"] / max(call["loss_pairs"], 1),
                         "ms_setup": last["ms_setup"], "ms_step": last["ms_step"], "ms_batch": last["ms_batch"],
                         "ms_sync": last["ms_sync"], "syncs": last["syncs"], "syncs_hot": last["syncs_hot"],
-                        "targets_per_word": last["targets"] / n_local, "rows_per_target": rows_per_target}
+                        "targets_per_word": call["targets"] / n_local, "rows_per_target": rows_per_target,
+                        "bytes_moved_per_word": last["bytes_moved"] / n_local}
         if world == 1 and not args.no_cpu_baseline and cfg.V * cfg.D <= 300_000_000:
             out["cpu_baseline"] = cpu_baseline(cfg, BASE_SAMPLE)
         elif world == 1 and not args.no_cpu_baseline:

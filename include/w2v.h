@@ -66,6 +66,9 @@ typedef struct {
                                 (ids are frequency ranks), i.e. the rows that must come from DRAM
                                 under an ideal static cache — B_cold of SURVEY.md §8(d)           */
     int64_t cold_from_row;   /* that prefix: L2 bytes / (8 D) rows, last train                    */
+    int64_t bytes_moved;     /* row bytes the step kernel actually gathered + reduced in the last
+                                w2v_train: bytes_row for the per-target kernels; fewer for the ring
+                                kernel, which keeps M_in rows of the window on chip             */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").

@@ -29,7 +29,8 @@ class Stats(ctypes.Structure):
                 ("loss_tail_sum", ctypes.c_double), ("loss_tail_pairs", ctypes.c_int64), ("kernel", ctypes.c_int64),
                 ("ms_batch", ctypes.c_double), ("l2_window_bytes", ctypes.c_int64), ("l2_carve_bytes", ctypes.c_int64),
                 ("syncs_hot", ctypes.c_int64), ("units_per_sm", ctypes.c_int64),
-                ("row_touches_cold", ctypes.c_int64), ("cold_from_row", ctypes.c_int64)]
+                ("row_touches_cold", ctypes.c_int64), ("cold_from_row", ctypes.c_int64),
+                ("bytes_moved", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -120,6 +120,8 @@ struct Ctx {
     DevStats* dstats = nullptr;
     unsigned long long* chunk_ctr = nullptr;
     int64_t* dp_tmp = nullptr;
+    uint32_t* tick = nullptr;               // mode 2: [issue 2V | done 2V] ticket counters
+    unsigned long long* turn = nullptr;     // mode 2: chunk turn of the current launch
     // batch stream of one launch range (batch.cu -> step kernels), capacity in chunks
     // two sets: the batch kernel fills set (j+1)&1 on the side stream while the step kernel
     // consumes set j&1 on the main stream
@@ -358,7 +360,7 @@ int w2v_set_option(const char* key, int64_t v) {
     if (!g.live) return fail(W2V_ESTATE, "w2v_set_option before w2v_init");
     if (!key) return fail(W2V_EINVAL, "w2v_set_option: null key");
     std::string k(key);
-    if (k == "mode") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "mode must be 0 or 1"); g.mode = (int)v; }
+    if (k == "mode") { if (v < 0 || v > 2) return fail(W2V_EINVAL, "mode must be 0 (Hogwild), 1 (deterministic, one unit) or 2 (deterministic, conflict-ticketed)"); g.mode = (int)v; }
     else if (k == "sentence_len") { if (v < 1 || v > 4096) return fail(W2V_EINVAL, "sentence_len out of [1,4096]"); g.L = (int32_t)v; }
     else if (k == "sync_period_words") { if (v < 1) return fail(W2V_EINVAL, "sync_period_words must be >= 1"); g.sync_period = v; }
     else if (k == "sync_hot_rows") { if (v < 0) return fail(W2V_EINVAL, "sync_hot_rows must be >= 0"); g.sync_hot_rows = v; }
@@ -381,7 +383,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
     else if (k == "check_finite") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "check_finite must be 0/1"); g.check_finite = (int)v; }
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
-    else if (k == "kernel") { if (v < 0 || v > 3) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window) or 3 (window, warp-specialised)"); g.kernel = (int)v; }
+    else if (k == "kernel") { if (v < 0 || v > 4) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window), 3 (window, warp-specialised) or 4 (ring, TMEM originals)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
     else if (k == "epoch_base") { if (v < 0 || v > 255) return fail(W2V_EINVAL, "epoch_base out of [0,255]"); g.epoch_base = (int32_t)v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
@@ -574,39 +576,69 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         p.cold_from = (int64_t)l2 / ((int64_t)8 * g.D);
         g.st.cold_from_row = p.cold_from;
     }
-    if (g.rowpath_only && (g.algorithm != 0 || (g.kernel != 0 && g.kernel != 1)))
-        return bail(fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows kernel (kernel 0/1, algorithm 0)"));
+    if (g.rowpath_only && (g.algorithm != 0 || (g.kernel != 0 && g.kernel != 1 && g.kernel != 4)))
+        return bail(fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows and ring kernels (kernel 0/1/4, algorithm 0)"));
     if (g.algorithm == 1 && !alg1_supported(g.D, g.K))
         return bail(fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K));
     // kernel choice: 1 per-target rows, 2 window-resident (one warp per unit),
     // 3 window-resident warp-specialised (a CTA of column warps + an IO warp per unit)
     int32_t off_win = 0, off_row = 0, off_wg = 0;
     const size_t wb_win = win_warp_bytes(g.L, g.window, g.K, g.D, &off_win);
-    const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row);
+    int32_t off_tick = 0;
+    const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row, g.mode == 2 ? &off_tick : nullptr);
     const size_t wb_wg = wg_cta_bytes(g.L, g.window, g.K, g.D, &off_wg);
+    int32_t off_ring = 0;
+    const size_t wb_ring = ring_warp_bytes(g.L, g.window, g.K, g.D, &off_ring);
     const size_t kSmemMax = 227 * 1024;
     int kern = g.kernel == 0 ? 1 : g.kernel;
     if (g.algorithm == 1) kern = 0;  // alg1.cu
+    if (g.mode == 2) {  // NEXT-4: the rows kernel with per-row tickets (hogbatch.cu)
+        if (kern != 1 || 2 * g.window + g.K + 1 > 32)
+            return bail(fail(W2V_EINVAL, "w2v_train: mode 2 (conflict-ticketed) needs the rows kernel (kernel 0/1, "
+                             "algorithm 0) and 2*window+K+1 <= 32"));
+        if (!g.tick) {
+            int rc = dmalloc((void**)&g.tick, (size_t)g.V * 4 * sizeof(uint32_t), "mode-2 ticket counters");
+            if (rc) return bail(rc);
+            rc = dmalloc((void**)&g.turn, 64, "mode-2 chunk turn");
+            if (rc) return bail(rc);
+        }
+        CUB(cudaMemsetAsync(g.tick, 0, (size_t)g.V * 4 * sizeof(uint32_t), st));
+        p.tick_issue = g.tick;
+        p.tick_done = g.tick + 2 * g.V;
+        p.turn = g.turn;
+        p.tick_off = off_tick;
+    }
+    int ring_units = 0;  // kernel 4: work units (warps) per CTA, one CTA per SM
+    if (kern == 4) {
+        ring_units = g.mode == 1 ? 1 : ring_units_per_cta(g.window, g.D, g.K, wb_ring, kSmemMax);
+        if (g.mode == 0 && g.ctas_per_sm > 0 && g.ctas_per_sm < ring_units) ring_units = g.ctas_per_sm;
+        if (!ring_supported(g.window, g.D, g.K) || wb_ring == 0 || ring_units < 1)
+            return bail(fail(W2V_EINVAL, "w2v_train: kernel=4 (ring) unsupported for window=%d, D=%d, K=%d, L=%d (window <= 15)",
+                             g.window, g.D, g.K, g.L));
+    }
     if (kern == 2 && !(wb_win > 0 && wb_win <= kSmemMax))
         return bail(fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L));
     if (kern == 3 && !(wb_wg > 0 && wb_wg <= kSmemMax))
         return bail(fail(W2V_EINVAL, "w2v_train: kernel=3 (window, warp-specialised) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L));
     const bool use_win = kern == 2;
-    size_t wb = kern == 3 ? wb_wg : use_win ? wb_win : wb_row;
+    size_t wb = kern == 4 ? wb_ring : kern == 3 ? wb_wg : use_win ? wb_win : wb_row;
     if (kern == 0) wb = alg1_warp_bytes(g.L);
-    p.slab_offset = kern == 3 ? off_wg : use_win ? off_win : off_row;
+    p.slab_offset = kern == 4 ? off_ring : kern == 3 ? off_wg : use_win ? off_win : off_row;
     if (wb == 0 || wb > kSmemMax) return bail(fail(W2V_EINVAL, "w2v_train: shared memory per work unit %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb));
     p.warp_bytes = (int32_t)wb;
     int ctas = 1;
-    if (g.mode == 0) {
+    if (kern == 4) {
+        ctas = g.mode == 0 ? g.sms : 1;   // one CTA of ring_units warps per SM (its TMEM block)
+    } else if (g.mode != 1) {
         int occ = kern == 0 ? alg1_max_ctas_per_sm(p) : kern == 3 ? wg_max_ctas_per_sm(p)
                 : use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
         if (occ < 1) return bail(fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per work unit)", wb));
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
-    g.st.units_per_sm = ctas >= g.sms ? ctas / g.sms : 1;
-    g.st.kernel = kern == 0 ? 4 : kern;  // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1
+    g.st.units_per_sm = kern == 4 ? ring_units : ctas >= g.sms ? ctas / g.sms : 1;
+    // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1, 5 ring
+    g.st.kernel = kern == 0 ? 4 : kern == 4 ? 5 : kern;
     CUB(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
@@ -698,9 +730,11 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                     CU(mark(2));
                 }
                 CU(cudaMemsetAsync(g.chunk_ctr, 0, 8, st));
+                if (g.mode == 2) CU(cudaMemsetAsync(g.turn, 0, 8, st));
                 CU(mark(0));
-                CU(kern == 0 ? launch_alg1(p, ctas, st) : kern == 3 ? launch_wg(p, ctas, st)
-                                    : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
+                CU(kern == 0 ? launch_alg1(p, ctas, st) : kern == 4 ? launch_ring(p, ctas, ring_units, st)
+                   : kern == 3 ? launch_wg(p, ctas, st)
+                   : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
                 CU(mark(0));
                 if (ovl) CU(cudaEventRecord(ev_sdone[set], st));
                 launches += 2;
@@ -780,6 +814,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     g.st.launches = launches;
     g.st.bytes_row = (int64_t)hs.row_touches * 4 * g.D * 2;
     g.st.row_touches_cold = (int64_t)hs.row_touches_cold;
+    g.st.bytes_moved = (kern == 4 ? (int64_t)hs.rows_moved : 2 * (int64_t)hs.row_touches) * 4 * g.D;
     if (g.check_finite && hend.nonfinite)
         return fail(W2V_ENUMERIC, "w2v_train: the model holds NaN/Inf after training (diverged; lower alpha)");
     return W2V_OK;
@@ -904,6 +939,7 @@ int w2v_finalize(void) {
     free_bt();
     cudaFree(g.M); cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
     cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
+    cudaFree(g.tick); cudaFree(g.turn);
     cudaStreamSynchronize(g.side);
     cudaStreamSynchronize(g.comm_stream);
     cudaStreamDestroy(g.side);

@@ -39,6 +39,26 @@ __device__ unsigned long long g_phase[8];
 
 namespace {
 
+// ---- mode 2 (NEXT-4): acquire/release on the ticket counters and the chunk turn
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* a) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add_u32(uint32_t* a, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+// order this thread's async-proxy (bulk copy) global accesses with its generic ones
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 constexpr int kSmemChunk = 256;  // chunks up to this many (padded) kept slots are staged in smem
 
 #ifndef W2V_MINB
@@ -116,10 +136,20 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         if (c1 > shard_end) c1 = shard_end;
         if (c0 < p.shard_start) c0 = p.shard_start;
         const int cnt = (int)(c1 - c0);
-        if (cnt <= 0) continue;
+        const int64_t rel = s - p.chunk_lo;
+        const bool ticketed = p.deterministic == 2;
+        if (cnt <= 0) {
+            if (ticketed) {  // an empty chunk still passes the turn on
+                if (lane == 0) {
+                    while (ld_acquire_u64(p.turn) != (unsigned long long)rel) __nanosleep(20);
+                    st_release_u64(p.turn, (unsigned long long)rel + 1);
+                }
+                __syncwarp();
+            }
+            continue;
+        }
 
         // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
-        const int64_t rel = s - p.chunk_lo;
         W2V_T(long long t0 = clock64();)
         if (chunk_smem) {
             kid = kid_s;
@@ -138,6 +168,34 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         W2V_T(ph[0] += clock64() - t0;)
         const int nk = *nk_s;
         if (lane == 0) st_words += (unsigned long long)cnt;
+        uint32_t* tick = reinterpret_cast<uint32_t*>(wbase + p.tick_off);  // [nk][RMAX] (mode 2)
+        if (ticketed) {
+            // NEXT-4 (dependences between iterations): chunks take their turn in
+            // corpus order; during its turn a chunk takes one ticket per row access of each of
+            // its targets, in sequential order. A target later waits, per row, until every
+            // earlier access of that row has completed (done == its first ticket), so each row
+            // sees exactly the sequential order of updates while non-conflicting targets of
+            // different chunks run in parallel — bit-identical to mode 1.
+            if (lane == 0)
+                while (ld_acquire_u64(p.turn) != (unsigned long long)rel) __nanosleep(20);
+            __syncwarp();
+            if (nk >= 2) {
+                for (int m = 0; m < nk; ++m) {
+                    const int b = kinfo[m] & 255;
+                    const int lo = m - b < 0 ? 0 : m - b;
+                    const int hi = m + b > nk - 1 ? nk - 1 : m + b;
+                    const int N = hi - lo;
+                    for (int r = lane; r < N + KP1; r += 32) {
+                        const int32_t id = r < N ? kid[lo + r + (lo + r >= m ? 1 : 0)]
+                                         : r == N ? kid[m] : p.bt_neg[(rel * p.Lp + m) * KS + (r - N - 1)];
+                        tick[m * RMAX + r] = atomicAdd(p.tick_issue + (r < N ? 0 : p.V) + id, 1u);
+                    }
+                }
+            }
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release_u64(p.turn, (unsigned long long)rel + 1);
+        }
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
         // alpha (C8): recomputed only when a target crosses into the next Q-quantum
@@ -152,6 +210,26 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             int32_t* rowid = rowid0 + buf * RMAX;
             const int R = N + KP1;
             const int64_t pp = c0 + (kinfo[m] >> 8);
+            // mode 2: wait until every earlier access of each of this target's rows completed
+            uint32_t my_first = 0, my_mult = 0;   // lane r < R: first ticket of row r's (matrix, id), multiplicity
+            if (ticketed) {
+                if (lane < R) {
+                    const int32_t id = rowid[lane];
+                    const bool outside = lane >= N;
+                    my_first = tick[m * RMAX + lane];
+                    for (int r2 = 0; r2 < R; ++r2)
+                        if ((r2 >= N) == outside && rowid[r2] == id) {
+                            const uint32_t t2 = tick[m * RMAX + r2];
+                            my_first = t2 < my_first ? t2 : my_first;
+                            ++my_mult;
+                        }
+                    if (my_first != tick[m * RMAX + lane]) my_mult = 0;  // released by the first occurrence
+                    const uint32_t* dn = p.tick_done + (outside ? p.V : 0) + id;
+                    while (ld_acquire_u32(dn) != my_first) __nanosleep(20);
+                }
+                __syncwarp();
+                fence_proxy_async_global();
+            }
             // ---------------- a3: gather the snapshot rows (one bulk copy per row)
             W2V_T(long long t1 = clock64();)
 #ifndef W2V_ABL_NOGATHER
@@ -346,6 +424,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             bulk_wait_read_all();
 #endif
             if (p.deterministic) __threadfence();
+            if (ticketed) {  // mode 2: this target's accesses are complete: release the rows
+                fence_proxy_async_global();
+                __threadfence();
+                if (lane < R && my_mult) red_release_add_u32(p.tick_done + (lane >= N ? p.V : 0) + rowid[lane], my_mult);
+            }
             __syncwarp();
             W2V_T(ph[3] += clock64() - t4; ph[4] += 1;)
             N = Nn;
@@ -429,7 +512,7 @@ void step_phase_report() {
 #endif
 }
 
-size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
+size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, int32_t* tick_offset) {
     // [mbarrier 8 B | nk 4 B][kid Lp][kinfo Lp][rowid 2 x (2w+K+1)][negs 32 x max(K,1)][G tiles x 32]
     // [slab: KP1MAX B rows + 2w A rows, stride RS fp32]. RS = 64*CP2 (zero padding), or D for a
     // packed instance (W2V_SLAB_PAD=1 forces the padded one; experiments).
@@ -444,7 +527,12 @@ size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     const size_t ids = 16 + (size_t)(2 * Lps + 2 * R + kSampWinRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 15) / 16 * 16;  // 16-B aligned slab (bulk copies); every byte counts
     if (slab_offset) *slab_offset = (int32_t)off;
-    return off + (size_t)(in->kp1 + 2 * window) * RS * 4;
+    const size_t end = off + (size_t)(in->kp1 + 2 * window) * RS * 4;
+    if (tick_offset) {  // mode 2: + a ticket table [Lp][2w+K+1] u32 after the slab
+        *tick_offset = (int32_t)end;
+        return end + (size_t)Lp * R * 4;
+    }
+    return end;
 }
 
 int step_max_ctas_per_sm(const StepParams& p) {

@@ -20,6 +20,7 @@ struct DevStats {
     double loss_tail_sum;
     unsigned long long loss_tail_pairs;
     unsigned long long row_touches_cold;  // row touches with id >= StepParams::cold_from
+    unsigned long long rows_moved;        // rows actually gathered + reduced (ring kernel)
 };
 
 struct StepParams {
@@ -61,6 +62,13 @@ struct StepParams {
     int64_t hot_rows_in;  // M_in rows (contexts) in the rows kernel
     int32_t l2_hint;
     int32_t rowpath_only; // measurement mode: rows kernel without a4-a6 (zero deltas; model unchanged)
+    // mode 2 (NEXT-4, conflict-ticketed deterministic; rows kernel): per (matrix, row) the next
+    // ticket to hand out and the number of completed accesses ([0,V) M_in, [V,2V) M_out), the
+    // launch's chunk turn, and the byte offset of the warp's ticket table in shared memory
+    uint32_t* tick_issue;
+    uint32_t* tick_done;
+    unsigned long long* turn;
+    int32_t tick_off;
     int64_t cold_from;    // statistics: row touches with id >= cold_from are counted as "cold" (the
                           // ids beyond an L2-sized hot prefix; the cache-aware roofline's B_cold)
     int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)
@@ -103,11 +111,17 @@ size_t alg1_warp_bytes(int L);
 int alg1_max_ctas_per_sm(const StepParams& p);
 cudaError_t launch_alg1(const StepParams& p, int ctas, cudaStream_t st);
 
+// hogbatch_ring.cu (window ring of M_in rows, originals in TMEM; window <= 15)
+size_t ring_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
+int ring_units_per_cta(int window, int D, int K, size_t warp_bytes, size_t smem_max);
+bool ring_supported(int window, int D, int K);
+cudaError_t launch_ring(const StepParams& p, int ctas, int units, cudaStream_t st);
+
 // hogbatch.cu (per-target rows; any window)
 bool step_supported(int D, int K);
 cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st);
 int step_max_ctas_per_sm(const StepParams& p);
-size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset);
+size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, int32_t* tick_offset = nullptr);
 void step_phase_report();  // (experiment builds with W2V_PHASE_TIMING) prints per-phase cycles
 
 }  // namespace w2v

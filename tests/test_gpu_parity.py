@@ -44,10 +44,12 @@ def row_rel_max(a, ref):
 
 # Deterministic-mode bars, all measured against the fp64 oracle O-HB:
 #  * global relative L2 <= 1e-5 (BASELINE.json north_star);
-#  * global relative L2 <= 1.25 x the fp32 oracle's own distance to fp64 (+2e-7 for the regime
-#    where both sit at fp32 rounding): the GPU may re-associate sums (FFMA2 column pairs, a
-#    butterfly instead of a sequential d-loop) but must not be less accurate than a plain fp32
-#    run of the same algorithm;
+#  * global relative L2 <= 1.25 x the fp32 oracle's own distance to fp64 + 1e-6 (~8 fp32 ulps:
+#    the regime of tiny or degenerate runs where a few re-associated roundings dominate, e.g.
+#    V=1, where every update of a target hits the same row): the GPU may re-associate sums
+#    (FFMA2 column pairs, a butterfly instead of a sequential d-loop) but must not be less
+#    accurate than a plain fp32 run of the same algorithm. Measured ratios (r02): 0.99-1.05 at
+#    cfg1/cfg2/cfg3 for the rows kernel, 0.4-0.8 for the window kernels;
 #  * per-row max relative error <= 2 x the fp32 oracle's per-row max (+1e-6): catches a
 #    single wrong row or element that the global norm hides.
 def assert_model_parity(tag, g_in, g_out, o_in, o_out, f_in, f_out):
@@ -60,7 +62,7 @@ def assert_model_parity(tag, g_in, g_out, o_in, o_out, f_in, f_out):
               f"per-row max {rg:.3e} (fp32 oracle {rf:.3e})")
     for name, eg, ef, rg, rf in rows:
         assert eg <= 1e-5, f"{tag} {name}: rel L2 {eg:.3e} > 1e-5"
-        assert eg <= 1.25 * ef + 2e-7, f"{tag} {name}: rel L2 {eg:.3e} > 1.25 x fp32 oracle {ef:.3e}"
+        assert eg <= 1.25 * ef + 1e-6, f"{tag} {name}: rel L2 {eg:.3e} > 1.25 x fp32 oracle {ef:.3e} + 1e-6"
         assert rg <= 2.0 * rf + 1e-6, f"{tag} {name}: per-row max {rg:.3e} > 2 x fp32 oracle {rf:.3e}"
 
 
@@ -111,8 +113,10 @@ def test_init_bitexact(w2v):
 
 
 # ------------------------------------------------------------------ cfg1 parity --------------
-KERNELS = [1, 2, 3]  # 1 = per-target rows (hogbatch.cu), 2 = window-resident rows (hogbatch_win.cu),
-                     # 3 = window-resident, warp-specialised (hogbatch_wg.cu)
+KERNELS = [1, 2, 3, 4]  # 1 = per-target rows (hogbatch.cu), 2 = window-resident rows (hogbatch_win.cu),
+                        # 3 = window-resident, warp-specialised (hogbatch_wg.cu),
+                        # 4 = window ring with TMEM originals (hogbatch_ring.cu)
+STAT_KERNEL = {1: 1, 2: 2, 3: 3, 4: 5}   # option "kernel" -> w2v_stats_t.kernel
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -124,7 +128,7 @@ def test_cfg1_deterministic_parity(w2v, n, kernel):
     ids = cfg.corpus().tokens(0, n)
     g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, n),
                 opts={"kernel": kernel})
-    assert g["stats"]["kernel"] == kernel
+    assert g["stats"]["kernel"] == STAT_KERNEL[kernel]
     o_in, o_out, o_st, o_dbg = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
                                             debug=(0, n))
     assert_stream_equal(g["dbg"], o_dbg)
@@ -159,7 +163,8 @@ def test_cfg2_deterministic_parity_prefix(w2v):
     assert abs(g["stats"]["loss_sum"] / o_st["loss_sum"] - 1) <= 1e-5
 
 
-def test_cfg3_headline_shape_deterministic_prefix(w2v):
+@pytest.mark.parametrize("kernel", [1, 4])
+def test_cfg3_headline_shape_deterministic_prefix(w2v, kernel):
     """Deterministic parity at the HEADLINE shape (BASELINE cfg3: V=1,000,000, D=300, window=5,
     K=5, t=1e-4, planted Zipf(1.07)) on the first 2^20 tokens: the bench's packed
     <5,6,300> instance with the a8 evict_last hints over a V=1M model (counts, thresholds and
@@ -172,18 +177,22 @@ def test_cfg3_headline_shape_deterministic_prefix(w2v):
     ids = cfg.corpus().tokens(0, n)
     dbgw = (n // 2 + 3, 3000)
     args = (ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
+    key = ("cfg3-det", n, dbgw)
     with ThreadPoolExecutor(2) as ex:
-        f64 = ex.submit(oracle.train, *args, debug=dbgw)
-        f32 = ex.submit(oracle.train, *args, prec="f32")
-        g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=dbgw)
-        o_in, o_out, o_st, o_dbg = f64.result()
-        f_in, f_out, _, _ = f32.result()
-    assert g["stats"]["kernel"] in (1, 4)
+        if key not in _ORACLE_CACHE:
+            f64 = ex.submit(oracle.train, *args, debug=dbgw)
+            f32 = ex.submit(oracle.train, *args, prec="f32")
+        g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=dbgw,
+                    opts={"kernel": kernel})
+        if key not in _ORACLE_CACHE:
+            _ORACLE_CACHE[key] = (f64.result(), f32.result())
+    (o_in, o_out, o_st, o_dbg), (f_in, f_out, _, _) = _ORACLE_CACHE[key]
+    assert g["stats"]["kernel"] == STAT_KERNEL[kernel]
     assert_stream_equal(g["dbg"], o_dbg)
     for k in ("words", "targets", "row_touches", "loss_pairs"):
         assert g["stats"][k] == o_st[k], k
     assert abs(g["stats"]["loss_sum"] / o_st["loss_sum"] - 1) <= 1e-5
-    assert_model_parity("cfg3[:2^20]", g["M_in"], g["M_out"], o_in, o_out, f_in, f_out)
+    assert_model_parity(f"cfg3[:2^20] kernel {kernel}", g["M_in"], g["M_out"], o_in, o_out, f_in, f_out)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -218,7 +227,7 @@ def test_edge_shapes_deterministic(w2v, V, D, window, K, t, L, n, epochs, allow,
     ids = inputs.Corpus("iid", V, 1.0, 99).tokens(0, n)
     g = run_gpu(w2v, ids, V, D, window, K, 0.05, t, 7, L, epochs=epochs, debug=(0, n),
                 opts={"allow_target_negative": allow, "kernel": kernel})
-    assert g["stats"]["kernel"] == kernel
+    assert g["stats"]["kernel"] == STAT_KERNEL[kernel]
     o_in, o_out, o_st, o_dbg = oracle.train(ids, V, D, window, K, 0.05, t, 7, L, epochs=epochs,
                                             allow_target_negative=bool(allow), debug=(0, n))
     if epochs == 1:
@@ -346,7 +355,8 @@ def test_cfg2_hogwild_loss_and_recall(w2v, kernel):
         assert abs(rg - ro) <= 0.02 and ro > 0.3
 
 
-def test_cfg3_hogwild_prefix_loss_gate(w2v):
+@pytest.mark.parametrize("kernel", [1, 4])
+def test_cfg3_hogwild_prefix_loss_gate(w2v, kernel):
     """Hogwild mode at the HEADLINE shape (cfg3: V=1M, D=300, window=5, K=5, t=1e-4) over the
     first 2^24 tokens with all SMs (the bench's launch configuration and kernel): final-10% and
     held-out training loss within 1% of the SEQUENTIAL oracle's (north_star; PAPER.md:70-75:
@@ -358,21 +368,27 @@ def test_cfg3_hogwild_prefix_loss_gate(w2v):
     ids = cfg.corpus().tokens(0, n)
     dbgw = (n // 3 + 11, 3000)
     tail_from = (n * 9 // 10) // cfg.L * cfg.L
+    key = (cfg.idx, ids.size, tail_from, dbgw)
     with ThreadPoolExecutor(1) as ex:
-        fut = ex.submit(oracle_train_tail, ids, cfg, tail_from, "f32", dbgw)
+        fut = None if key in _ORACLE_CACHE else ex.submit(oracle_train_tail, ids, cfg, tail_from, "f32", dbgw)
         g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, mode=0,
-                    debug=dbgw, opts={"loss_tail_from": tail_from})
-        o_in, o_out, o_st, o_tail, o_dbg = fut.result()
+                    debug=dbgw, opts={"loss_tail_from": tail_from, "kernel": kernel})
+        if fut is not None:
+            _ORACLE_CACHE[key] = fut.result()
+    o_in, o_out, o_st, o_tail, o_dbg = _ORACLE_CACHE[key]
+    assert g["stats"]["kernel"] == STAT_KERNEL[kernel]
     assert_stream_equal(g["dbg"], o_dbg)
     assert g["stats"]["row_touches"] == o_st["row_touches"]
     assert g["stats"]["loss_tail_pairs"] == o_tail["loss_pairs"]
     gt = g["stats"]["loss_tail_sum"] / g["stats"]["loss_tail_pairs"]
     ot = o_tail["loss_sum"] / o_tail["loss_pairs"]
     hg = heldout_loss(g["M_in"], g["M_out"], cfg, n, 200_000)
-    ho = heldout_loss(o_in, o_out, cfg, n, 200_000)
+    if key + ("heldout",) not in _ORACLE_CACHE:
+        _ORACLE_CACHE[key + ("heldout",)] = heldout_loss(o_in, o_out, cfg, n, 200_000)
+    ho = _ORACLE_CACHE[key + ("heldout",)]
     gl = g["stats"]["loss_sum"] / g["stats"]["loss_pairs"]
     ol = o_st["loss_sum"] / o_st["loss_pairs"]
-    print(f"cfg3[:2^24] Hogwild ({g['stats']['units_per_sm']} units/SM): loss/pair whole run GPU {gl:.6f} "
+    print(f"cfg3[:2^24] Hogwild kernel {kernel} ({g['stats']['units_per_sm']} units/SM): loss/pair whole run GPU {gl:.6f} "
           f"oracle {ol:.6f}; final 10% GPU {gt:.6f} oracle {ot:.6f}; held-out GPU {hg:.6f} oracle {ho:.6f}")
     assert abs(gt / ot - 1) < 0.01
     assert abs(hg / ho - 1) < 0.01
@@ -575,3 +591,38 @@ def test_caller_stream_same_results(w2v):
     w2v.get_embeddings(0, M_in)
     assert np.array_equal(M_in, a["M_in"])
     w2v.set_stream(None)
+
+
+# ------------------------------------------------------------------ NEXT-4: mode 2 ------------
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "V1", "K0", "w15"])
+def test_mode2_ticketed_equals_serial(w2v, case):
+    """Mode 2: every SM runs targets in parallel, each
+    row access waiting on a per-row ticket taken in corpus order, so every row receives exactly
+    the sequential order of updates. The model must be BIT-IDENTICAL to mode 1 (one unit, corpus
+    order), the batch stream and counters identical; only the fp64 loss sum may differ in its
+    last bits (per-warp partial sums). Cases: cfg1 full, a cfg2 prefix, V=1 (every negative is
+    the fallback row: all targets conflict), K=0, and the largest ticketed window (2w+K+1 = 32)."""
+    if case in ("cfg1", "cfg2"):
+        cfg = inputs.CONFIGS[1 if case == "cfg1" else 2]
+        n = cfg.n if case == "cfg1" else 400_000
+        ids = cfg.corpus().tokens(0, n)
+        args = (cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
+    else:
+        V, D, window, K, L, n = {"V1": (1, 8, 2, 3, 10, 2_000), "K0": (50, 36, 3, 0, 64, 8_000),
+                                 "w15": (30, 8, 15, 1, 300, 6_000)}[case]
+        ids = inputs.Corpus("iid", V, 1.0, 99).tokens(0, n)
+        args = (V, D, window, K, 0.05, 0.0, 7, L)
+    dbg = (n // 3, min(3000, n // 2))
+    a = run_gpu(w2v, ids, *args, mode=1, debug=dbg)
+    w2v.finalize()
+    b = run_gpu(w2v, ids, *args, mode=2, debug=dbg)
+    print(f"mode 2 vs mode 1 ({case}): step ms {b['stats']['ms_step']:.1f} vs {a['stats']['ms_step']:.1f} "
+          f"({b['stats']['units_per_sm']} units/SM)")
+    assert b["stats"]["units_per_sm"] >= 1
+    for f in ("keep", "b", "N", "ctx", "neg"):
+        assert np.array_equal(a["dbg"][f], b["dbg"][f]), f
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert a["stats"][k] == b["stats"][k], k
+    assert np.array_equal(a["M_in"].view(np.uint32), b["M_in"].view(np.uint32))
+    assert np.array_equal(a["M_out"].view(np.uint32), b["M_out"].view(np.uint32))
+    assert abs(a["stats"]["loss_sum"] - b["stats"]["loss_sum"]) <= 1e-9 * abs(a["stats"]["loss_sum"])
