@@ -85,7 +85,11 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
 
 /* Set an integer option before w2v_train (SURVEY.md §5 "Config / flags"). Keys:
  *  "mode"                  0 = Hogwild (default), 1 = deterministic
- *                          (one work unit, targets in corpus order, R17)
+ *                          (one work unit, targets in corpus order, R17), 2 = deterministic
+ *                          and parallel ("dependence
+ *                          between iterations"): all SMs, every row access waits on a per-row
+ *                          ticket taken in corpus order — bit-identical to mode 1 (rows kernel,
+ *                          2*window+K+1 <= 32)
  *  "sentence_len"          chunk length L of C5 (1..4096; default 1000)
  *  "sync_period_words"     P of C13 (>=1; default 2^20)
  *  "sync_hot_rows"         C14: rows [0,H) of both matrices (the Zipf-hot prefix)
@@ -119,7 +123,11 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          launch's duration; results do not depend on it in deterministic mode
  *  "kernel"                0 auto (default), 1 per-target rows (hogbatch.cu),
  *                          2 window-resident rows (hogbatch_win.cu; window <= 15), 3 window-
- *                          resident warp-specialised (hogbatch_wg.cu; window <= 15)
+ *                          resident warp-specialised (hogbatch_wg.cu; window <= 15), 4 window
+ *                          ring with the originals in tensor memory (hogbatch_ring.cu; window
+ *                          <= 15): ~1 gather + 1 reduction per kept position for M_in
+ *  "ring_writeback"        kernel 4 in deterministic mode: 0 (default) stores the slot value
+ *                          (the exact sequential row), 1 reduces slot - original as Hogwild does
  *  "check_finite"          1 (default): scan the model for NaN/Inf after every w2v_train (one
  *                          streaming pass, ~0.5 ms at cfg3) and return W2V_ENUMERIC if found
  *  "overlap_batch"         1: the a1/a2 batch kernel of launch j+1 runs on a side stream
@@ -142,7 +150,8 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
 int w2v_set_option(const char* key, int64_t value);
 
 /* Use this CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream) for all
- * subsequent work; NULL restores the library's private stream. */
+ * subsequent work; NULL restores the library's private stream. Plumbing, not a step of the
+ * method (PyTorch supplies device memory, streams and process groups). */
 int w2v_set_stream(void* cuda_stream);
 
 /* Train (PAPER.md:116-126 HogBatch; PAPER.md:135-138 Hogwild across work units).
@@ -160,11 +169,15 @@ int w2v_train(const int32_t* corpus_ids, int64_t n_tokens, int32_t epochs);
  * ranks (R13). World 1: no-op. */
 int w2v_sync(void);
 
-/* Copy M_in (which = 0) or M_out (which = 1) into dst, V x D fp32 row-major, host or device. */
+/* Copy M_in (which = 0) or M_out (which = 1) into dst, V x D fp32 row-major, host or device.
+ * M_in / M_out are the input and output embedding matrices of the problem statement
+ * (Alg.1 l.1 "model parameter Omega = {M_in, M_out}"); M_in is the
+ * word embedding (R15). Errors: ESTATE before w2v_init, EINVAL for which not 0/1 or dst NULL. */
 int w2v_get_embeddings(int32_t which, float* dst);
 
 /* Overwrite M_in (which = 0) or M_out (which = 1) from src, V x D fp32 row-major, host or
- * device (resume / test setup). */
+ * device (resume / test setup): the same Omega restored from a checkpoint
+ * (SURVEY.md §5). Errors as w2v_get_embeddings. */
 int w2v_set_embeddings(int32_t which, const float* src);
 
 /* Statistics of the last w2v_train (counters are cumulative since w2v_init; ms_* and
@@ -172,7 +185,8 @@ int w2v_set_embeddings(int32_t which, const float* src);
 int w2v_get_stats(w2v_stats_t* out);
 
 /* Copy the batch stream recorded by the last w2v_train for [debug_base, debug_base+debug_len)
- * (C5-C7): keep u8[len], b u8[len] (0 = not kept), N u8[len] (0 = not trained), ctx
+ * (C5-C7: the subsampling, window and negative-sampling decisions of Alg.1 l.3-11,
+ * PAPER.md:41-49, as shared per target by HogBatch): keep u8[len], b u8[len] (0 = not kept), N u8[len] (0 = not trained), ctx
  * int32[len][2*window] (-1 padded), neg int32[len][max(K,1)] (-1 padded). Host or device;
  * any pointer may be NULL. ESTATE if nothing was recorded. */
 int w2v_debug_batches(uint8_t* keep, uint8_t* b, uint8_t* N, int32_t* ctx, int32_t* neg);

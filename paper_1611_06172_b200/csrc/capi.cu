@@ -107,6 +107,7 @@ struct Ctx {
     int kernel = 0;  // 0 auto, 1 per-target rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
     int algorithm = 0;  // 0 HogBatch, 1 Alg.1 (alg1.cu)
     int rowpath_only = 0;  // measurement mode of the rows kernel (StepParams::rowpath_only)
+    int ring_writeback = 0;  // ring kernel, deterministic mode: 0 store the slot, 1 reduce slot - original
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -381,6 +382,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
     else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
+    else if (k == "ring_writeback") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "ring_writeback must be 0/1"); g.ring_writeback = (int)v; }
     else if (k == "check_finite") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "check_finite must be 0/1"); g.check_finite = (int)v; }
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 4) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window), 3 (window, warp-specialised) or 4 (ring, TMEM originals)"); g.kernel = (int)v; }
@@ -570,6 +572,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.dbg_a1neg = g.dbg_a1neg;
     p.algorithm = g.algorithm;
     p.rowpath_only = g.rowpath_only;
+    p.ring_delta = g.ring_writeback;
     {   // cache-aware roofline statistics: the hot prefix whose half-rows of both matrices fill L2
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g.device);

@@ -125,9 +125,9 @@ uint32_t pow2_cols(uint32_t c) {
 // CP2 = float2 columns per lane (D <= 64*CP2); KP1MAX >= K+1; RSC: packed smem row stride (0 =
 // padded to 64*CP2). One WARP = one work unit; a CTA holds `units` of them and one TMEM block.
 template <int CP2, int KP1MAX, int RSC>
-// 184 registers x 32 lanes x 11 warps = 64,768 of the SM's 65,536 (a 352-thread __launch_bounds__
-// would make ptxas budget for 384 threads: 168 registers and more spills)
-__global__ void __maxnreg__(184) hogbatch_ring_kernel(const StepParams p, int units_cols) {
+// registers are partitioned per SM sub-partition (16,384 each): 11 warps put 3 on some
+// sub-partitions, so <= 170 per thread (168; the rows kernel's budget too)
+__global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(const StepParams p, int units_cols) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int TI = 32 / KP1MAX;  // inputs per reduce-scatter tile
     constexpr int NC = 2 * CP2;      // TMEM columns per slot (the lane's floats of one row)
@@ -439,7 +439,12 @@ __global__ void __maxnreg__(184) hogbatch_ring_kernel(const StepParams p, int un
                     if (__shfl_sync(kFull, left, sl)) outm |= 1u << sl;
                 }
             }
-            for (uint32_t om = outm; om; om &= om - 1) {   // delta = slot - original, in place
+            // write-back of the leaving slots. Hogwild: delta = slot - original (TMEM), reduced
+            // into the row so concurrent units' updates survive. Deterministic (one unit, no
+            // concurrent writer) with option ring_writeback = 0: the slot VALUE is stored, exactly
+            // the sequential row (bit-identical to the rows kernel's mode 1)
+            const bool store_back = p.deterministic && !p.ring_delta;
+            for (uint32_t om = store_back ? 0u : outm; om; om &= om - 1) {   // delta = slot - original, in place
                 const int sl = __ffs(om) - 1;
                 float v[NC];
                 tmem_load_row<NC>(tbase + (uint32_t)(sl * NC), v);
@@ -462,8 +467,11 @@ __global__ void __maxnreg__(184) hogbatch_ring_kernel(const StepParams p, int un
                 bulk_red_add_s2g_hint(p.M + (size_t)oid * 2 * Ds + Ds, Bs + lane * RS, rowbytes,
                                       oid < p.hot_rows ? pol_hot : pol_cold);
             if ((outm >> lane) & 1u) {
-                bulk_red_add_s2g_hint(p.M + (size_t)slot_word * 2 * Ds, Ring + lane * RS, rowbytes,
-                                      slot_word < p.hot_rows_in ? pol_hot : pol_cold);
+                if (store_back)
+                    bulk_s2g(p.M + (size_t)slot_word * 2 * Ds, Ring + lane * RS, rowbytes);
+                else
+                    bulk_red_add_s2g_hint(p.M + (size_t)slot_word * 2 * Ds, Ring + lane * RS, rowbytes,
+                                          slot_word < p.hot_rows_in ? pol_hot : pol_cold);
                 slot_word = -1;
             }
             bulk_commit();

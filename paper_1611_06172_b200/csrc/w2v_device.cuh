@@ -127,6 +127,11 @@ __device__ __forceinline__ void bulk_red_add_s2g_hint(float* gdst, const void* s
                  "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
                  : "memory");
 }
+// shared -> global plain copy (bulk_group completion)
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
 // bring [gsrc, gsrc+bytes) into L2 ahead of use (bytes multiple of 16, 16-B aligned)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");

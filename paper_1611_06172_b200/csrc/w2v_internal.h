@@ -69,6 +69,8 @@ struct StepParams {
     uint32_t* tick_done;
     unsigned long long* turn;
     int32_t tick_off;
+    int32_t ring_delta;   // ring kernel, deterministic mode: 1 = write back slot - original
+                          // (the Hogwild path) instead of the slot value (option ring_writeback)
     int64_t cold_from;    // statistics: row touches with id >= cold_from are counted as "cold" (the
                           // ids beyond an L2-sized hot prefix; the cache-aware roofline's B_cold)
     int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)

@@ -626,3 +626,56 @@ def test_mode2_ticketed_equals_serial(w2v, case):
     assert np.array_equal(a["M_in"].view(np.uint32), b["M_in"].view(np.uint32))
     assert np.array_equal(a["M_out"].view(np.uint32), b["M_out"].view(np.uint32))
     assert abs(a["stats"]["loss_sum"] - b["stats"]["loss_sum"]) <= 1e-9 * abs(a["stats"]["loss_sum"])
+
+
+# ------------------------------------------------------------------ ring kernel (kernel 4) ----
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "V1", "w15", "D512"])
+def test_ring_deterministic_equals_rows_kernel(w2v, case):
+    """Kernel 4 (window ring, hogbatch_ring.cu) in deterministic mode keeps each window row in
+    shared memory, applies the targets' ΔIn to it in order and stores the slot back when the
+    position leaves: the exact sequential row. So its model must be BIT-IDENTICAL to the rows
+    kernel's deterministic run (which re-gathers every row per target), batch stream and
+    counters equal — across repeated words sharing a slot (V=1, window 15) and D=512."""
+    if case in ("cfg1", "cfg2"):
+        cfg = inputs.CONFIGS[1 if case == "cfg1" else 2]
+        n = cfg.n if case == "cfg1" else 200_000
+        ids = cfg.corpus().tokens(0, n)
+        args = (cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
+    else:
+        V, D, window, K, L, n = {"V1": (1, 8, 2, 3, 10, 2_000), "w15": (30, 8, 15, 1, 300, 6_000),
+                                 "D512": (40, 512, 2, 4, 4096, 4_100)}[case]
+        ids = inputs.Corpus("iid", V, 1.0, 99).tokens(0, n)
+        args = (V, D, window, K, 0.05, 0.0, 7, L)
+    dbg = (n // 3, min(3000, n // 2))
+    a = run_gpu(w2v, ids, *args, mode=1, debug=dbg, opts={"kernel": 1})
+    w2v.finalize()
+    b = run_gpu(w2v, ids, *args, mode=1, debug=dbg, opts={"kernel": 4})
+    assert b["stats"]["kernel"] == 5
+    for f in ("keep", "b", "N", "ctx", "neg"):
+        assert np.array_equal(a["dbg"][f], b["dbg"][f]), f
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert a["stats"][k] == b["stats"][k], k
+    assert np.array_equal(a["M_in"].view(np.uint32), b["M_in"].view(np.uint32))
+    assert np.array_equal(a["M_out"].view(np.uint32), b["M_out"].view(np.uint32))
+    # the ring moves fewer row bytes than the algorithmic N+K+1 rows per target
+    assert b["stats"]["bytes_moved"] < a["stats"]["bytes_moved"] == 2 * 4 * args[1] * a["stats"]["row_touches"]
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2"])
+def test_ring_delta_writeback_parity(w2v, case):
+    """Kernel 4's Hogwild write-back path in a deterministic run (option ring_writeback=1): a
+    leaving slot is reduced into its row as  slot - original, the original read back from
+    tensor memory (tcgen05.st on entry, tcgen05.ld on leaving). One extra rounding per write-back
+    (exact when slot/original is in [1/2, 2]), so the model bars of assert_model_parity apply
+    against the fp64 oracle rather than bit-identity."""
+    cfg = inputs.CONFIGS[1 if case == "cfg1" else 2]
+    n = cfg.n if case == "cfg1" else 300_000
+    ids = cfg.corpus().tokens(0, n)
+    g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                opts={"kernel": 4, "ring_writeback": 1})
+    o_in, o_out, o_st, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
+    f_in, f_out, _, _ = oracle.train(ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L,
+                                     prec="f32")
+    for k in ("words", "targets", "row_touches", "loss_pairs"):
+        assert g["stats"][k] == o_st[k], k
+    assert_model_parity(f"{case}[:{n}] ring delta write-back", g["M_in"], g["M_out"], o_in, o_out, f_in, f_out)
