@@ -286,6 +286,8 @@ def run_ours(args):
     ovl = int(args.sync_overlap > 0)
     w2v.set_option("sync_overlap", ovl)
     w2v.set_option("kernel", args.kernel)
+    if args.scatter_wait >= 0:
+        w2v.set_option("scatter_wait", args.scatter_wait)
     w2v.set_option("algorithm", 1 if args.algorithm == "alg1" else 0)
     stream = torch.cuda.current_stream()
     w2v.set_stream(stream.cuda_stream)
@@ -467,6 +469,9 @@ def main():
     ap.add_argument("--sync-cold-every", type=int, default=1,
                     help="C14 cold rows averaged every this many intervals (1 = every interval: C13)")
     ap.add_argument("--sync-overlap", type=int, default=0, help="C15 overlapped averaging (1 = on)")
+    ap.add_argument("--scatter-wait", type=int, default=-1,
+                    help="1: each target waits for its reductions to complete (R11); 0: only until read "
+                         "(Hogwild staleness inside a chunk); -1: library default")
     ap.add_argument("--algorithm", choices=["hogbatch", "alg1"], default="hogbatch",
                     help="alg1: the paper's level-1 baseline (PAPER.md:37-63), for the HogBatch/Alg.1 ratio")
     args = ap.parse_args()

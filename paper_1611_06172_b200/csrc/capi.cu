@@ -107,7 +107,8 @@ struct Ctx {
     int kernel = 0;  // 0 auto, 1 per-target rows (hogbatch.cu), 2 window-resident (hogbatch_win.cu)
     int algorithm = 0;  // 0 HogBatch, 1 Alg.1 (alg1.cu)
     int rowpath_only = 0;  // measurement mode of the rows kernel (StepParams::rowpath_only)
-    int ring_writeback = 0;  // ring kernel, deterministic mode: 0 store the slot, 1 reduce slot - original
+    int ring_writeback = 0;
+    int scatter_wait = 1;    // StepParams::scatter_wait  // ring kernel, deterministic mode: 0 store the slot, 1 reduce slot - original
     // device state
     cudaStream_t own_stream = nullptr, stream = nullptr;
     float* M = nullptr;  // V rows of [M_in | M_out]
@@ -382,11 +383,12 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "loss_tail_from") { if (v < 0) return fail(W2V_EINVAL, "loss_tail_from must be >= 0"); g.loss_tail_from = v; }
     else if (k == "algorithm") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "algorithm must be 0 (HogBatch) or 1 (Alg.1)"); g.algorithm = (int)v; }
     else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
+    else if (k == "scatter_wait") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "scatter_wait must be 0/1"); g.scatter_wait = (int)v; }
     else if (k == "ring_writeback") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "ring_writeback must be 0/1"); g.ring_writeback = (int)v; }
     else if (k == "check_finite") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "check_finite must be 0/1"); g.check_finite = (int)v; }
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 4) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window), 3 (window, warp-specialised) or 4 (ring, TMEM originals)"); g.kernel = (int)v; }
-    else if (k == "launch_words") { if (v < 1) return fail(W2V_EINVAL, "launch_words must be >= 1"); g.launch_words = v; }
+    else if (k == "launch_words") { if (v < 1 || v > (1ll << 31)) return fail(W2V_EINVAL, "launch_words out of [1, 2^31]"); g.launch_words = v; }
     else if (k == "epoch_base") { if (v < 0 || v > 255) return fail(W2V_EINVAL, "epoch_base out of [0,255]"); g.epoch_base = (int32_t)v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
     else return fail(W2V_EINVAL, "w2v_set_option: unknown key '%s'", key);
@@ -573,6 +575,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.algorithm = g.algorithm;
     p.rowpath_only = g.rowpath_only;
     p.ring_delta = g.ring_writeback;
+    p.scatter_wait = g.scatter_wait;
     {   // cache-aware roofline statistics: the hot prefix whose half-rows of both matrices fill L2
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g.device);

@@ -419,7 +419,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             // the next target's gather must see these updates (R11: targets of a chunk are
             // sequential) and the slab must be free: wait for the reductions to complete
 #if !defined(W2V_ABL_NOWAIT)
-            bulk_wait_all();
+            // (option scatter_wait = 0, Hogwild only: wait just until the sources are read; see
+            // hogbatch_ring.cu)
+            if (p.deterministic || p.scatter_wait) bulk_wait_all();
+            else bulk_wait_read_all();
 #else
             bulk_wait_read_all();
 #endif

@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
     __syncwarp();
     uint32_t phase = 0;
 
-    unsigned long long st_words = 0, st_targets = 0, st_touch = 0, st_pairs = 0, st_tail_pairs = 0, st_moved = 0;
+    // per-warp counters of one launch; 32 bits where a launch (launch_words <= 2^31 raw words, one
+    // unit in deterministic mode) cannot overflow them
+    unsigned st_words = 0, st_targets = 0, st_touch = 0;
+    unsigned long long st_pairs = 0, st_tail_pairs = 0, st_moved = 0;
     unsigned st_cold = 0;
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
         cp_async_wait_all();
         __syncwarp();
         const int nk = *nk_s;
-        if (lane == 0) st_words += (unsigned long long)cnt;
+        if (lane == 0) st_words += (unsigned)cnt;
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
         // ring state, in registers: lane s < S holds slot s (word id, reference count); lane
@@ -368,28 +371,13 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                     if (valid) st_loss_f += fmaxf(pos ? -dot : dot, 0.f) - __logf(rc);
                 }
                 __syncwarp();
-                // ΔOut_j = Σ_i G_ij A_i over the SNAPSHOT (before any slot changes: two contexts
-                // may share a slot when a word repeats inside the window)
-                for (int i = 0; i < N; ++i) {
-                    const int slt = __shfl_sync(kFull, my_cs, i);
-                    const float* Ai = Ring + slt * RS + 2 * lane;
-                    float2 a[CP2];
-#pragma unroll
-                    for (int c = 0; c < CP2; ++c)
-                        a[c] = (c < CP2 - 1 || lastok) ? *reinterpret_cast<const float2*>(Ai + 64 * c) : make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int j = 0; j < KP1MAX; ++j) {
-                        const float gj = gs[i * KP1MAX + j];
-                        const float2 g2 = make_float2(gj, gj);
-#pragma unroll
-                        for (int c = 0; c < CP2; ++c) dq[j][c] = ffma2(g2, a[c], dq[j][c]);
-                    }
-                }
-                __syncwarp();
-                // slot(i) += ΔIn_i = Σ_j G_ij B_j, in input order (M_in[ctx_i] += ΔIn_i, C10)
-                for (int i = 0; i < N; ++i) {
-                    const int slt = __shfl_sync(kFull, my_cs, i);
-                    float* Ai = Ring + slt * RS + 2 * lane;
+                // a6 per input i: ΔOut_j += G_ij A_i (A over the SNAPSHOT) and slot(i) += ΔIn_i =
+                // Σ_j G_ij B_j, in input order (M_in[ctx_i] += ΔIn_i, C10). When a word repeats
+                // inside the window two contexts share a slot, and a later input must still read
+                // the snapshot: then all ΔOut first, all slot updates second
+                const unsigned dupm = __match_any_sync(kFull, lane < N ? my_cs : -1 - lane);
+                const bool dup = __any_sync(kFull, lane < N && __popc(dupm) > 1);
+                auto delta_in = [&](int i, float2 (&din)[CP2]) {
                     float2 g2[KP1MAX];
 #pragma unroll
                     for (int j = 0; j < KP1MAX; ++j) {
@@ -406,14 +394,50 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                         for (int j = 0; j < KP1MAX; ++j) s2[j % NCH] = ffma2(g2[j], bq[j][c], s2[j % NCH]);
 #pragma unroll
                         for (int h = 1; h < NCH; ++h) s2[0] = fadd2(s2[0], s2[h]);
-                        if (c < CP2 - 1 || lastok) {
-                            float2 x = *reinterpret_cast<float2*>(Ai + 64 * c);
-                            x.x = __fadd_rn(x.x, s2[0].x);
-                            x.y = __fadd_rn(x.y, s2[0].y);
-                            *reinterpret_cast<float2*>(Ai + 64 * c) = x;
-                        }
+                        din[c] = s2[0];
                     }
+                };
+                for (int i = 0; i < N; ++i) {
+                    const int slt = __shfl_sync(kFull, my_cs, i);
+                    float* Ai = Ring + slt * RS + 2 * lane;
+                    float2 a[CP2];
+#pragma unroll
+                    for (int c = 0; c < CP2; ++c)
+                        a[c] = (c < CP2 - 1 || lastok) ? *reinterpret_cast<const float2*>(Ai + 64 * c) : make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < KP1MAX; ++j) {
+                        const float gj = gs[i * KP1MAX + j];
+                        const float2 g2 = make_float2(gj, gj);
+#pragma unroll
+                        for (int c = 0; c < CP2; ++c) dq[j][c] = ffma2(g2, a[c], dq[j][c]);
+                    }
+                    if (!dup) {   // the common case: fused, A_i still in registers
+                        float2 din[CP2];
+                        delta_in(i, din);
+#pragma unroll
+                        for (int c = 0; c < CP2; ++c)
+                            if (c < CP2 - 1 || lastok)
+                                *reinterpret_cast<float2*>(Ai + 64 * c) =
+                                    make_float2(__fadd_rn(a[c].x, din[c].x), __fadd_rn(a[c].y, din[c].y));
+                    }
+                }
+                if (dup) {
                     __syncwarp();
+                    for (int i = 0; i < N; ++i) {
+                        const int slt = __shfl_sync(kFull, my_cs, i);
+                        float* Ai = Ring + slt * RS + 2 * lane;
+                        float2 din[CP2];
+                        delta_in(i, din);
+#pragma unroll
+                        for (int c = 0; c < CP2; ++c)
+                            if (c < CP2 - 1 || lastok) {
+                                float2 x = *reinterpret_cast<float2*>(Ai + 64 * c);
+                                x.x = __fadd_rn(x.x, din[c].x);
+                                x.y = __fadd_rn(x.y, din[c].y);
+                                *reinterpret_cast<float2*>(Ai + 64 * c) = x;
+                            }
+                        __syncwarp();
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < KP1MAX; ++j)
@@ -479,13 +503,13 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
             st_loss += (double)st_loss_f;
             if (pp >= p.loss_tail_from) {
                 st_tail += (double)st_loss_f;
-                if (lane == 0) st_tail_pairs += (unsigned long long)N * KP1;
+                if (lane == 0) st_tail_pairs += (unsigned long long)(N * KP1);
             }
             st_loss_f = 0.f;
             if (lane == 0) {
                 st_targets += 1;
-                st_touch += (unsigned long long)(N + KP1);
-                st_pairs += (unsigned long long)N * KP1;
+                st_touch += (unsigned)(N + KP1);
+                st_pairs += (unsigned long long)(N * KP1);
                 st_moved += (unsigned long long)(2 * KP1 + nnew + __popc(outm));
             }
             if (p.dbg_len && pp >= p.dbg_base && pp < p.dbg_base + p.dbg_len) {
@@ -495,7 +519,11 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                 for (int k = lane; k < K; k += 32) p.dbg_neg[qd * K + k] = ng[k];
             }
             // the next target's gathers must see these reductions (R11) and the slab must be free
-            bulk_wait_all();
+            // (option scatter_wait = 0, Hogwild only: just free — wait until the engine has read
+            // the sources; the chunk's next target may then read a row before this target's
+            // update to it lands, the same staleness Hogwild allows between units)
+            if (p.deterministic || p.scatter_wait) bulk_wait_all();
+            else bulk_wait_read_all();
             if (p.deterministic) __threadfence();
             __syncwarp();
         }
@@ -508,9 +536,9 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
         st_cold += __shfl_xor_sync(kFull, st_cold, o);
     }
     if (lane == 0) {
-        atomicAdd(&p.stats->words, st_words);
-        atomicAdd(&p.stats->targets, st_targets);
-        atomicAdd(&p.stats->row_touches, st_touch);
+        atomicAdd(&p.stats->words, (unsigned long long)st_words);
+        atomicAdd(&p.stats->targets, (unsigned long long)st_targets);
+        atomicAdd(&p.stats->row_touches, (unsigned long long)st_touch);
         atomicAdd(&p.stats->loss_pairs, st_pairs);
         atomicAdd(&p.stats->loss_sum, st_loss);
         atomicAdd(&p.stats->row_touches_cold, (unsigned long long)st_cold);

@@ -69,6 +69,8 @@ struct StepParams {
     uint32_t* tick_done;
     unsigned long long* turn;
     int32_t tick_off;
+    int32_t scatter_wait; // 1: a target waits for its reductions to complete before the next
+                          // target's gathers (R11); 0 (Hogwild only): until they are read
     int32_t ring_delta;   // ring kernel, deterministic mode: 1 = write back slot - original
                           // (the Hogwild path) instead of the slot value (option ring_writeback)
     int64_t cold_from;    // statistics: row touches with id >= cold_from are counted as "cold" (the
