@@ -71,7 +71,8 @@ constexpr int kSmemChunk = 256;  // chunks up to this many (padded) kept slots a
 // RSC: compile-time smem row stride of the slab (floats); 0 = padded to 64*CP2 (predicate-free).
 // The packed instance for the paper's D=300 (RSC=300) saves 20 floats per row — what lets an 11th
 // work unit fit per SM — at the cost of a predicate on each lane's last float2 column.
-template <int CP2, int KP1MAX, int RSC>
+// TK: the mode-2 (NEXT-4) ticketed instance; the others carry none of its code or registers
+template <int CP2, int KP1MAX, int RSC, bool TK>
 __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int TI = 32 / KP1MAX;  // inputs per reduce-scatter tile
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         if (c0 < p.shard_start) c0 = p.shard_start;
         const int cnt = (int)(c1 - c0);
         const int64_t rel = s - p.chunk_lo;
-        const bool ticketed = p.deterministic == 2;
+        constexpr bool ticketed = TK;
         if (cnt <= 0) {
             if (ticketed) {  // an empty chunk still passes the turn on
                 if (lane == 0) {
@@ -465,10 +466,10 @@ using KernelFn = void (*)(const StepParams);
 
 struct Inst {
     int cp2, kp1, rs;  // rs: packed row stride (the instance serves D == rs only), 0 = padded
-    KernelFn fn;
+    KernelFn fn, fn_tk;  // Hogwild / mode 1, and the mode-2 (ticketed) instance
 };
 
-#define W2V_INST(C, KK) {C, KK, 0, hogbatch_step_kernel<C, KK, 0>}
+#define W2V_INST(C, KK) {C, KK, 0, hogbatch_step_kernel<C, KK, 0, false>, hogbatch_step_kernel<C, KK, 0, true>}
 // (float2 columns per lane, max K+1) instantiations; register tile ~ 4*CP2*KP1MAX floats.
 const Inst kInst[] = {
     W2V_INST(1, 2), W2V_INST(1, 4), W2V_INST(1, 6), W2V_INST(1, 8), W2V_INST(1, 16), W2V_INST(1, 32),
@@ -477,7 +478,7 @@ const Inst kInst[] = {
     W2V_INST(4, 2), W2V_INST(4, 4), W2V_INST(4, 6), W2V_INST(4, 8),
     W2V_INST(5, 2), W2V_INST(5, 4), W2V_INST(5, 6), W2V_INST(5, 8),
     W2V_INST(8, 2), W2V_INST(8, 4), W2V_INST(8, 6),
-    {5, 6, 300, hogbatch_step_kernel<5, 6, 300>},  // the paper's D=300, K<=5, packed rows
+    {5, 6, 300, hogbatch_step_kernel<5, 6, 300, false>, hogbatch_step_kernel<5, 6, 300, true>},  // D=300, K<=5, packed
 };
 // Supported envelope (w2v_init rejects the rest): ceil(D/64) float2 columns per lane times
 // the padded K+1 tile must be one of the rows above, i.e. D <= 64 with K <= 31; D <= 128 with
@@ -541,18 +542,20 @@ size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, in
 int step_max_ctas_per_sm(const StepParams& p) {
     const Inst* in = pick(p.D, p.K);
     if (!in) return 0;
+    const KernelFn fn = p.deterministic == 2 ? in->fn_tk : in->fn;
     int n = 0;
-    cudaFuncSetAttribute(in->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.warp_bytes);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, in->fn, 32, p.warp_bytes) != cudaSuccess) return 0;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.warp_bytes);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, 32, p.warp_bytes) != cudaSuccess) return 0;
     return n;
 }
 
 cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st) {
     const Inst* in = pick(p.D, p.K);
     if (!in) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(in->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.warp_bytes);
+    const KernelFn fn = p.deterministic == 2 ? in->fn_tk : in->fn;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.warp_bytes);
     if (e != cudaSuccess) return e;
-    in->fn<<<ctas, 32, p.warp_bytes, st>>>(p);
+    fn<<<ctas, 32, p.warp_bytes, st>>>(p);
     return cudaGetLastError();
 }
 
