@@ -350,7 +350,7 @@ def run_ours(args):
     # row-path roof: the same kernel and batch stream with a4-a6 skipped (zero deltas reduced,
     # model unchanged) — what the gathers + scatters alone sustain on this chip
     roof = None
-    if args.algorithm == "hogbatch" and args.kernel in (0, 1, 4, 5) and not args.no_rowpath:
+    if args.algorithm == "hogbatch" and args.kernel in (0, 1, 4) and not args.no_rowpath:
         w2v.set_option("rowpath_only", 1)
         w2v.train(dev, n_local, 1)
         rs = w2v.get_stats()
@@ -379,7 +379,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, world),
             "run": {"units_per_sm": last["units_per_sm"], "mode": "hogwild",
-                    "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1", 5: "ring", 6: "rows-2warp"}.get(last["kernel"]),
+                    "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1", 5: "ring"}.get(last["kernel"]),
                     "step_launches_per_step": last["step_launches"]},
             # per call the library reads back its setup info (32 B) before training and its
             # statistics (72 B) + finite-check flag block (32 B) after it
@@ -459,7 +459,7 @@ def main():
     ap.add_argument("--no-rowpath", action="store_true", help="skip the rowpath_only roof run")
     ap.add_argument("--kernel", type=int, default=0,
                     help="0 auto, 1 per-target rows, 2 window-resident rows, 3 window-resident warp-specialised, "
-                         "4 ring (window-resident M_in rows, originals in TMEM), 5 rows with two warps per unit")
+                         "4 ring (window-resident M_in rows, originals in TMEM)")
     ap.add_argument("--tokens", type=int, default=0, help="profiling only: train on a prefix of the config")
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=CFG,
                     help="BASELINE.json config (3 = the headline workload; 4, 5 = the larger-tile / 4M-vocab ones)")

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libw2v.so")
 BUILD = os.path.join(PKG, "build")
-SOURCES = ["setup.cu", "batch.cu", "hogbatch.cu", "hogbatch_ring.cu", "hogbatch_pair.cu", "hogbatch_win.cu", "hogbatch_wg.cu", "alg1.cu", "sync.cu", "capi.cu"]
+SOURCES = ["setup.cu", "batch.cu", "hogbatch.cu", "hogbatch_ring.cu", "hogbatch_win.cu", "hogbatch_wg.cu", "alg1.cu", "sync.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # IEEE division/sqrt are required for the bit-exact contract (C2, C9): no fast-math.
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

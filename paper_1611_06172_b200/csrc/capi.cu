@@ -387,7 +387,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "ring_writeback") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "ring_writeback must be 0/1"); g.ring_writeback = (int)v; }
     else if (k == "check_finite") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "check_finite must be 0/1"); g.check_finite = (int)v; }
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
-    else if (k == "kernel") { if (v < 0 || v > 5) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window), 3 (window, warp-specialised), 4 (ring, TMEM originals) or 5 (rows, two warps per unit)"); g.kernel = (int)v; }
+    else if (k == "kernel") { if (v < 0 || v > 4) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window), 3 (window, warp-specialised) or 4 (ring, TMEM originals)"); g.kernel = (int)v; }
     else if (k == "launch_words") { if (v < 1 || v > (1ll << 31)) return fail(W2V_EINVAL, "launch_words out of [1, 2^31]"); g.launch_words = v; }
     else if (k == "epoch_base") { if (v < 0 || v > 255) return fail(W2V_EINVAL, "epoch_base out of [0,255]"); g.epoch_base = (int32_t)v; }
     else if (k == "epochs_total") { if (v < 0) return fail(W2V_EINVAL, "epochs_total must be >= 0"); g.epochs_total = (int32_t)v; }
@@ -583,7 +583,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         g.st.cold_from_row = p.cold_from;
     }
     if (g.rowpath_only && (g.algorithm != 0 || g.kernel == 2 || g.kernel == 3))
-        return bail(fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows, ring and two-warp kernels (kernel 0/1/4/5, algorithm 0)"));
+        return bail(fail(W2V_EINVAL, "w2v_train: rowpath_only applies to the rows and ring kernels (kernel 0/1/4, algorithm 0)"));
     if (g.algorithm == 1 && !alg1_supported(g.D, g.K))
         return bail(fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K));
     // kernel choice: 1 per-target rows, 2 window-resident (one warp per unit),
@@ -593,9 +593,8 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     int32_t off_tick = 0;
     const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row, g.mode == 2 ? &off_tick : nullptr);
     const size_t wb_wg = wg_cta_bytes(g.L, g.window, g.K, g.D, &off_wg);
-    int32_t off_ring = 0, off_pair = 0;
+    int32_t off_ring = 0;
     const size_t wb_ring = ring_warp_bytes(g.L, g.window, g.K, g.D, &off_ring);
-    const size_t wb_pair = pair_cta_bytes(g.L, g.window, g.K, g.D, &off_pair);
     const size_t kSmemMax = 227 * 1024;
     int kern = g.kernel == 0 ? 1 : g.kernel;
     if (g.algorithm == 1) kern = 0;  // alg1.cu
@@ -627,27 +626,25 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         return bail(fail(W2V_EINVAL, "w2v_train: kernel=2 (window) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L));
     if (kern == 3 && !(wb_wg > 0 && wb_wg <= kSmemMax))
         return bail(fail(W2V_EINVAL, "w2v_train: kernel=3 (window, warp-specialised) unsupported for window=%d, D=%d, K=%d, L=%d", g.window, g.D, g.K, g.L));
-    if (kern == 5 && !(pair_supported(g.D, g.K) && wb_pair > 0 && wb_pair <= kSmemMax))
-        return bail(fail(W2V_EINVAL, "w2v_train: kernel=5 (two warps per unit) unsupported for D=%d, K=%d", g.D, g.K));
     const bool use_win = kern == 2;
-    size_t wb = kern == 5 ? wb_pair : kern == 4 ? wb_ring : kern == 3 ? wb_wg : use_win ? wb_win : wb_row;
+    size_t wb = kern == 4 ? wb_ring : kern == 3 ? wb_wg : use_win ? wb_win : wb_row;
     if (kern == 0) wb = alg1_warp_bytes(g.L);
-    p.slab_offset = kern == 5 ? off_pair : kern == 4 ? off_ring : kern == 3 ? off_wg : use_win ? off_win : off_row;
+    p.slab_offset = kern == 4 ? off_ring : kern == 3 ? off_wg : use_win ? off_win : off_row;
     if (wb == 0 || wb > kSmemMax) return bail(fail(W2V_EINVAL, "w2v_train: shared memory per work unit %zu B exceeds 227 KB (reduce sentence_len/window/K/D)", wb));
     p.warp_bytes = (int32_t)wb;
     int ctas = 1;
     if (kern == 4) {
         ctas = g.mode == 0 ? g.sms : 1;   // one CTA of ring_units warps per SM (its TMEM block)
     } else if (g.mode != 1) {
-        int occ = kern == 0 ? alg1_max_ctas_per_sm(p) : kern == 5 ? pair_max_ctas_per_sm(p) : kern == 3 ? wg_max_ctas_per_sm(p)
+        int occ = kern == 0 ? alg1_max_ctas_per_sm(p) : kern == 3 ? wg_max_ctas_per_sm(p)
                 : use_win ? win_max_ctas_per_sm(p) : step_max_ctas_per_sm(p);
         if (occ < 1) return bail(fail(W2V_ECUDA, "w2v_train: step kernel cannot be resident (%zu B smem per work unit)", wb));
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
     g.st.units_per_sm = kern == 4 ? ring_units : ctas >= g.sms ? ctas / g.sms : 1;
-    // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1, 5 ring, 6 rows with two warps
-    g.st.kernel = kern == 0 ? 4 : kern == 4 ? 5 : kern == 5 ? 6 : kern;
+    // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1, 5 ring
+    g.st.kernel = kern == 0 ? 4 : kern == 4 ? 5 : kern;
     CUB(cudaMemsetAsync(g.dstats, 0, sizeof(DevStats), st));
     const Plan pl = make_plan(n_global, g.L, g.world, g.rank, g.sync_period);
     const int64_t chunk_lo = shard_start / g.L;
@@ -742,7 +739,6 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 if (g.mode == 2) CU(cudaMemsetAsync(g.turn, 0, 8, st));
                 CU(mark(0));
                 CU(kern == 0 ? launch_alg1(p, ctas, st) : kern == 4 ? launch_ring(p, ctas, ring_units, st)
-                   : kern == 5 ? launch_pair(p, ctas, st)
                    : kern == 3 ? launch_wg(p, ctas, st)
                    : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
                 CU(mark(0));

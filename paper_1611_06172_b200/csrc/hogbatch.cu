@@ -60,6 +60,7 @@ __device__ __forceinline__ void red_release_add_u32(uint32_t* a, uint32_t v) {
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 constexpr int kSmemChunk = 256;  // chunks up to this many (padded) kept slots are staged in smem
+constexpr int kKRing = 128;      // long chunks: ring of kept slots (ids, offsets) in smem
 
 #ifndef W2V_MINB
 #define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for (the packed
@@ -86,8 +87,12 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     // kSmemChunk) are read in place from the batch stream (global, generic loads), which keeps a
     // unit's smem at the slab's size — at L = 1000 that is 8 KB, i.e. 3 more units per SM
     const bool chunk_smem = p.Lp <= kSmemChunk;
+    // long chunks with window <= 32: a ring of kKRing kept slots (ids and offsets), staged 32
+    // slots at a time by cp.async ahead of the targets that read them (an L2 round trip per
+    // slot on the critical path otherwise: DESIGN.md §8, cfg4)
+    const bool kring_on = !chunk_smem && window <= 32;
     int32_t* kid_s = reinterpret_cast<int32_t*>(wbase + 16);
-    const int Lps = chunk_smem ? p.Lp : 0;
+    const int Lps = chunk_smem ? p.Lp : kring_on ? kKRing : 0;
     int32_t* rowid0 = kid_s + 2 * Lps;                        // 2 x RMAX: ctx ids, target, negatives
     int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWinRows x KS negatives ring
     float* gs = reinterpret_cast<float*>(negs + kSampWinRows * KS);  // G of the target, [N][KP1MAX]
@@ -114,15 +119,26 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     double st_loss = 0.0, st_tail = 0.0;
 
     // ---- C6: context ids, target and its (already sampled) negatives of kept target m
-    const int32_t* kid = kid_s;    // set per chunk (smem or the batch stream)
+    const int32_t* kid = kid_s;    // set per chunk: the whole chunk in smem, the ring, or global
     const int32_t* kinfo = kid_s + Lps;
+    int kmask = -1;                // slot index mask (kKRing - 1 for the ring)
+    const int32_t* kid_g = nullptr;    // the chunk's kept list in the batch stream (global)
+    const int32_t* kinfo_g = nullptr;
+    int kb_hi = 0;                 // ring: 32-slot blocks staged so far
+    auto stage_block = [&](int blk) {  // ring: slots [32 blk, 32 blk + 32) of ids and offsets
+        const int q = 32 * blk + 4 * (lane & 7);
+        if (lane < 16 && q < p.Lp) {
+            const int32_t* src = (lane < 8 ? kid_g : kinfo_g) + q;
+            cp_async16(kid_s + (lane < 8 ? 0 : kKRing) + (q & (kKRing - 1)), src);
+        }
+    };
     auto gather_list = [&](int m, int nk, int32_t* rowid) -> int {
-        const int b = kinfo[m] & 255;
+        const int b = kinfo[m & kmask] & 255;
         const int lo = m - b < 0 ? 0 : m - b;
         const int hi = m + b > nk - 1 ? nk - 1 : m + b;
         const int N = hi - lo;
-        for (int i = lane; i < N; i += 32) rowid[i] = kid[lo + i + (lo + i >= m ? 1 : 0)];
-        if (lane == 0) rowid[N] = kid[m];
+        for (int i = lane; i < N; i += 32) rowid[i] = kid[(lo + i + (lo + i >= m ? 1 : 0)) & kmask];
+        if (lane == 0) rowid[N] = kid[m & kmask];
         const int32_t* ng = negs + (m % kSampWinRows) * KS;
         for (int k = lane; k < K; k += 32) rowid[N + 1 + k] = ng[k];
         return N;
@@ -152,15 +168,26 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 
         // ---------------- the chunk's batch stream (a1/a2 rows, batch.cu)
         W2V_T(long long t0 = clock64();)
+        kid_g = p.bt_kid + rel * p.Lp;
+        kinfo_g = p.bt_kinfo + rel * p.Lp;
         if (chunk_smem) {
             kid = kid_s;
             kinfo = kid_s + Lps;
+            kmask = -1;
         } else {
-            kid = p.bt_kid + rel * p.Lp;
-            kinfo = p.bt_kinfo + rel * p.Lp;
             if (lane == 0) {  // the chunk's kept list, read target by target below, into L2 now
-                bulk_prefetch_l2(kid, (uint32_t)p.Lp * 4u);
-                bulk_prefetch_l2(kinfo, (uint32_t)p.Lp * 4u);
+                bulk_prefetch_l2(kid_g, (uint32_t)p.Lp * 4u);
+                bulk_prefetch_l2(kinfo_g, (uint32_t)p.Lp * 4u);
+            }
+            if (kring_on) {   // first blocks: every slot gather_list(0) and (1) can read
+                kid = kid_s;
+                kinfo = kid_s + kKRing;
+                kmask = kKRing - 1;
+                for (kb_hi = 0; 32 * kb_hi < p.Lp && 32 * kb_hi <= window + 1; ++kb_hi) stage_block(kb_hi);
+            } else {
+                kid = kid_g;
+                kinfo = kinfo_g;
+                kmask = -1;
             }
         }
         load_chunk<kSampWinRows>(p, rel, chunk_smem ? kid_s : nullptr, kid_s + Lps, nk_s, negs, lane);
@@ -181,14 +208,16 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 while (ld_acquire_u64(p.turn) != (unsigned long long)rel) __nanosleep(20);
             __syncwarp();
             if (nk >= 2) {
+                const int32_t* kidx = chunk_smem ? kid_s : kid_g;   // the whole chunk
+                const int32_t* kinfx = chunk_smem ? kid_s + Lps : kinfo_g;
                 for (int m = 0; m < nk; ++m) {
-                    const int b = kinfo[m] & 255;
+                    const int b = kinfx[m] & 255;
                     const int lo = m - b < 0 ? 0 : m - b;
                     const int hi = m + b > nk - 1 ? nk - 1 : m + b;
                     const int N = hi - lo;
                     for (int r = lane; r < N + KP1; r += 32) {
-                        const int32_t id = r < N ? kid[lo + r + (lo + r >= m ? 1 : 0)]
-                                         : r == N ? kid[m] : p.bt_neg[(rel * p.Lp + m) * KS + (r - N - 1)];
+                        const int32_t id = r < N ? kidx[lo + r + (lo + r >= m ? 1 : 0)]
+                                         : r == N ? kidx[m] : p.bt_neg[(rel * p.Lp + m) * KS + (r - N - 1)];
                         tick[m * RMAX + r] = atomicAdd(p.tick_issue + (r < N ? 0 : p.V) + id, 1u);
                     }
                 }
@@ -210,7 +239,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         for (int m = 0; m < nk; ++m) {
             int32_t* rowid = rowid0 + buf * RMAX;
             const int R = N + KP1;
-            const int64_t pp = c0 + (kinfo[m] >> 8);
+            const int64_t pp = c0 + (kinfo[m & kmask] >> 8);
             // mode 2: wait until every earlier access of each of this target's rows completed
             uint32_t my_first = 0, my_mult = 0;   // lane r < R: first ticket of row r's (matrix, id), multiplicity
             if (ticketed) {
@@ -258,6 +287,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 fetch_negs<kSampWinRows>(p, rel, samp_hi, c, negs, lane);
                 samp_hi += c;
             }
+            // ring: stage the blocks up to slot m+2+w now — gather_list(m+2), one iteration on,
+            // reads up to there after this group completes; the oldest slot still read, m+1-w,
+            // stays within kKRing of the newest (window <= 32)
+            if (kring_on)
+                for (; 32 * kb_hi < nk && 32 * kb_hi <= m + 2 + window; ++kb_hi) stage_block(kb_hi);
             cp_async_commit();
             cp_async_wait_but_last();
             __syncwarp();
@@ -527,7 +561,8 @@ size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, in
     const int TI = 32 / in->kp1;
     const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
     const int Lp = (L + 3) & ~3;
-    const int Lps = Lp <= kSmemChunk ? Lp : 0;  // long chunks are read from the batch stream in place
+    // long chunks: a kKRing-slot ring (window <= 32), else read from the batch stream in place
+    const int Lps = Lp <= kSmemChunk ? Lp : window <= 32 ? kKRing : 0;
     const size_t ids = 16 + (size_t)(2 * Lps + 2 * R + kSampWinRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 15) / 16 * 16;  // 16-B aligned slab (bulk copies); every byte counts
     if (slab_offset) *slab_offset = (int32_t)off;

@@ -121,12 +121,6 @@ int ring_units_per_cta(int window, int D, int K, size_t warp_bytes, size_t smem_
 bool ring_supported(int window, int D, int K);
 cudaError_t launch_ring(const StepParams& p, int ctas, int units, cudaStream_t st);
 
-// hogbatch_pair.cu (two warps per unit, the K+1 outputs split between them; any window)
-bool pair_supported(int D, int K);
-size_t pair_cta_bytes(int L, int window, int K, int D, int32_t* slab_offset);
-int pair_max_ctas_per_sm(const StepParams& p);
-cudaError_t launch_pair(const StepParams& p, int ctas, cudaStream_t st);
-
 // hogbatch.cu (per-target rows; any window)
 bool step_supported(int D, int K);
 cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st);
