@@ -50,7 +50,8 @@ def main(tag, csv_path, rep, bench_log):
         for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             f.write(f"| `{k}` | {n} | {ms:.2f} | {100 * ms / tot:.2f}% |\n")
         f.write(f"\nBench (no profiler): kernel_share_of_step = {bench['roofline']['kernel_share_of_step']:.4f}, "
-                f"value = {bench['value'] / 1e6:.1f} M words/s, R_HBM = {bench['roofline']['frac']:.3f}.\n")
+                f"value = {bench['value'] / 1e6:.1f} M words/s, L2 row-path fraction = {bench['roofline']['frac']:.3f}, "
+                f"R_HBM = {bench['roofline_hbm']['frac']:.3f}.\n")
     s = ncu_summary.summary(rep)
     dram = float(s["dram__bytes_read.sum"][0]) + float(s["dram__bytes_write.sum"][0])
     unit = s["dram__bytes_read.sum"][1]
@@ -66,15 +67,19 @@ def main(tag, csv_path, rep, bench_log):
     lts_bpc = float(rd["lts__t_sectors.sum"]) * 32 / float(rd["lts__cycles_elapsed.avg"])
     traffic = {"dram_bytes_per_launch": dram_bytes, "words_per_launch": words,
                "dram_bytes_per_word": dram_bytes / words, "source": os.path.basename(rep), "round": tag,
-               "algorithmic_bytes_per_word": bench["roofline"]["row_bytes_per_word"],
+               "algorithmic_bytes_per_word": bench["roofline_hbm"]["row_bytes_per_word"],
                "config": int(os.environ.get("W2V_PROFILED_CONFIG", "3")), "kernel": "hogbatch_step (rows)",
-               "lts_bytes_per_cycle": lts_bpc}
-    cap = os.path.join(ROOT, "profiles", "l2cap.json")
+               "kernel_id": 1, "lts_bytes_per_cycle": lts_bpc,
+               "lts__t_sectors.sum": float(rd["lts__t_sectors.sum"]),
+               "lts__cycles_elapsed.avg": float(rd["lts__cycles_elapsed.avg"])}
+    cap = os.path.join(ROOT, "profiles", "r02_l2cap_ncu.json")
     if os.path.exists(cap):
         c = json.load(open(cap))
-        traffic["lts_cap_bytes_per_cycle"] = c["bulk_gather_reduce_lts_B_per_cycle"]
-        traffic["lts_cap_source"] = ("measured: tools/l2cap.cu, L2-resident bulk gather + bulk reduce of 1200-B rows "
-                                     "(the step's access pattern), profiles/l2cap.json")
+        best = max(x["lts_bytes_per_cycle"] for x in c["rowpath_cap_ncu"])
+        traffic["lts_cap_bytes_per_cycle"] = best
+        traffic["lts_frac_of_cap"] = lts_bpc / best
+        traffic["lts_cap_source"] = ("measured: tools/peaks.cu peaks_l2_rowpath under ncu (bulk gather of 11 rows + "
+                                     "bulk reduce, 1200-B rows, L2-resident; best residency), profiles/r02_l2cap_ncu.json")
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     json.dump({k: {"value": v, "unit": u} for k, (v, u) in s.items()},
               open(os.path.join(ROOT, "profiles", f"{tag}_hogbatch_step_ncu.json"), "w"), indent=1)
@@ -94,8 +99,12 @@ def main(tag, csv_path, rep, bench_log):
         for k, (v, u) in s.items():
             f.write(f"| {k} | {u} | {v} |\n")
         f.write(f"\nDRAM traffic per launch = {dram_bytes / 1e9:.1f} GB = {dram_bytes / words:.0f} B per raw word "
-                f"(algorithmic row bytes {bench['roofline']['row_bytes_per_word']:.0f} B/word: L2 serves "
-                f"{100 * (1 - dram_bytes / words / bench['roofline']['row_bytes_per_word']):.0f}% of the row traffic).\n")
+                f"(algorithmic row bytes {bench['roofline_hbm']['row_bytes_per_word']:.0f} B/word: L2 serves "
+                f"{100 * (1 - dram_bytes / words / bench['roofline_hbm']['row_bytes_per_word']):.0f}% of the row traffic).\n")
+        f.write(f"\nL2 slices: lts__t_sectors.sum = {float(rd['lts__t_sectors.sum']):.4g}, lts__cycles_elapsed.avg = "
+                f"{float(rd['lts__cycles_elapsed.avg']):.4g} -> {lts_bpc:.0f} B per L2 cycle chip-wide"
+                + (f" = {traffic['lts_frac_of_cap']:.3f} of the cap pattern's {traffic['lts_cap_bytes_per_cycle']:.0f} "
+                   f"(profiles/r02_l2cap_ncu.json)" if "lts_frac_of_cap" in traffic else "") + ".\n")
         f.write("\n## Warp-stall samples by source line (top 25)\n\n```\n" + lines_out + "```\n")
         f.write("\n## Executed instruction mix (SASS opcodes)\n\n```\n" + ops + "```\n")
     print(open(os.path.join(ROOT, "profiles", f"{tag}_launches.md")).read())
