@@ -60,7 +60,19 @@ __device__ __forceinline__ void red_release_add_u32(uint32_t* a, uint32_t v) {
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 constexpr int kSmemChunk = 256;  // chunks up to this many (padded) kept slots are staged in smem
-constexpr int kKRing = 128;      // long chunks: ring of kept slots (ids, offsets) in smem
+// long chunks: ring of kept slots (ids, offsets) in smem; it must span the 2w + 34 slots in use
+// (w+1 behind the reader, the staged block ahead): 64 for window <= 15, else 128 (window <= 32)
+// Staged 16 slots at a time; slots read at iteration m span [m+1-w, block end of m+2+w]:
+// 2w + 18 at most -> the smallest power of two >= 2w + 19 (32 at cfg5's window 5: a unit keeps
+// its 20.2 KB and 11 units fit per SM).
+constexpr int kKBlock = 16;
+// negatives of the next targets, staged by cp.async: a ring of 8 targets refilled 4 at a time
+// (load_chunk brings the first 8), so a target's group is >= 3 iterations old when it is read
+constexpr int kNegRows = 8;
+constexpr int kNegGrp = 4;
+__host__ __device__ constexpr int kring_slots(int window) {
+    return 2 * window + 19 <= 32 ? 32 : 2 * window + 19 <= 64 ? 64 : 128;
+}
 
 #ifndef W2V_MINB
 #define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for (the packed
@@ -87,15 +99,16 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     // kSmemChunk) are read in place from the batch stream (global, generic loads), which keeps a
     // unit's smem at the slab's size — at L = 1000 that is 8 KB, i.e. 3 more units per SM
     const bool chunk_smem = p.Lp <= kSmemChunk;
-    // long chunks with window <= 32: a ring of kKRing kept slots (ids and offsets), staged 32
+    // long chunks with window <= 32: a ring of kring_slots kept slots (ids and offsets), staged 16
     // slots at a time by cp.async ahead of the targets that read them (an L2 round trip per
     // slot on the critical path otherwise: DESIGN.md §8, cfg4)
     const bool kring_on = !chunk_smem && window <= 32;
     int32_t* kid_s = reinterpret_cast<int32_t*>(wbase + 16);
-    const int Lps = chunk_smem ? p.Lp : kring_on ? kKRing : 0;
+    const int KR = kring_slots(window);
+    const int Lps = chunk_smem ? p.Lp : kring_on ? KR : 0;
     int32_t* rowid0 = kid_s + 2 * Lps;                        // 2 x RMAX: ctx ids, target, negatives
-    int32_t* negs = rowid0 + 2 * RMAX;                        // kSampWinRows x KS negatives ring
-    float* gs = reinterpret_cast<float*>(negs + kSampWinRows * KS);  // G of the target, [N][KP1MAX]
+    int32_t* negs = rowid0 + 2 * RMAX;                        // kNegRows x KS negatives ring
+    float* gs = reinterpret_cast<float*>(negs + kNegRows * KS);  // G of the target, [N][KP1MAX]
     constexpr int RS = RSC > 0 ? RSC : 64 * CP2;             // smem row stride (floats)
     const bool lastok = RS >= 64 * CP2 || 2 * lane + 64 * (CP2 - 1) < D;  // lane's last float2 column exists
     float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
@@ -121,15 +134,15 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     // ---- C6: context ids, target and its (already sampled) negatives of kept target m
     const int32_t* kid = kid_s;    // set per chunk: the whole chunk in smem, the ring, or global
     const int32_t* kinfo = kid_s + Lps;
-    int kmask = -1;                // slot index mask (kKRing - 1 for the ring)
+    int kmask = -1;                // slot index mask (KR - 1 for the ring)
     const int32_t* kid_g = nullptr;    // the chunk's kept list in the batch stream (global)
     const int32_t* kinfo_g = nullptr;
     int kb_hi = 0;                 // ring: 32-slot blocks staged so far
-    auto stage_block = [&](int blk) {  // ring: slots [32 blk, 32 blk + 32) of ids and offsets
-        const int q = 32 * blk + 4 * (lane & 7);
-        if (lane < 16 && q < p.Lp) {
-            const int32_t* src = (lane < 8 ? kid_g : kinfo_g) + q;
-            cp_async16(kid_s + (lane < 8 ? 0 : kKRing) + (q & (kKRing - 1)), src);
+    auto stage_block = [&](int blk) {  // ring: slots [16 blk, 16 blk + 16) of ids and offsets
+        const int q = kKBlock * blk + 4 * (lane & 3);
+        if (lane < 8 && q < p.Lp) {
+            const int32_t* src = (lane < 4 ? kid_g : kinfo_g) + q;
+            cp_async16(kid_s + (lane < 4 ? 0 : KR) + (q & (KR - 1)), src);
         }
     };
     auto gather_list = [&](int m, int nk, int32_t* rowid) -> int {
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         const int N = hi - lo;
         for (int i = lane; i < N; i += 32) rowid[i] = kid[(lo + i + (lo + i >= m ? 1 : 0)) & kmask];
         if (lane == 0) rowid[N] = kid[m & kmask];
-        const int32_t* ng = negs + (m % kSampWinRows) * KS;
+        const int32_t* ng = negs + (m % kNegRows) * KS;
         for (int k = lane; k < K; k += 32) rowid[N + 1 + k] = ng[k];
         return N;
     };
@@ -181,16 +194,16 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             if (kring_on) {   // first blocks: every slot gather_list(0) and (1) can read
                 kid = kid_s;
-                kinfo = kid_s + kKRing;
-                kmask = kKRing - 1;
-                for (kb_hi = 0; 32 * kb_hi < p.Lp && 32 * kb_hi <= window + 1; ++kb_hi) stage_block(kb_hi);
+                kinfo = kid_s + KR;
+                kmask = KR - 1;
+                for (kb_hi = 0; kKBlock * kb_hi < p.Lp && kKBlock * kb_hi <= window + 1; ++kb_hi) stage_block(kb_hi);
             } else {
                 kid = kid_g;
                 kinfo = kinfo_g;
                 kmask = -1;
             }
         }
-        load_chunk<kSampWinRows>(p, rel, chunk_smem ? kid_s : nullptr, kid_s + Lps, nk_s, negs, lane);
+        load_chunk<kNegRows>(p, rel, chunk_smem ? kid_s : nullptr, kid_s + Lps, nk_s, negs, lane);
         cp_async_wait_all();
         __syncwarp();
         W2V_T(ph[0] += clock64() - t0;)
@@ -232,7 +245,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         int64_t q_next = -1;
         float alpha = 0.f;
 
-        int samp_hi = nk < kSampGrp ? nk : kSampGrp;  // negatives of [0, samp_hi) are in the ring
+        int samp_hi = nk < kNegRows ? nk : kNegRows;  // negatives of [0, samp_hi) are in the ring (load_chunk)
         int buf = 0;
         int N = gather_list(0, nk, rowid0);
         __syncwarp();
@@ -280,18 +293,20 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 #endif
             }
             // while the rows fly: fetch negatives ahead, build the next target's row list, alpha.
-            // One cp.async group per target (possibly empty); after iteration m the ring holds
-            // targets up to >= m+9, so waiting for all groups but this one covers target m+1.
-            if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kSampGrp) {
-                const int c = nk - samp_hi < kSampGrp ? nk - samp_hi : kSampGrp;
-                fetch_negs<kSampWinRows>(p, rel, samp_hi, c, negs, lane);
+            // One cp.async group per target (possibly empty); targets fetched at iteration m' are
+            // >= m'+4 (a group of 4 when fewer than 4 remain ahead of m'+1), so waiting for all
+            // groups but this one covers target m+1, and the 8-target ring never overwrites one
+            // before gather_list has read it.
+            if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kNegGrp) {
+                const int c = nk - samp_hi < kNegGrp ? nk - samp_hi : kNegGrp;
+                fetch_negs<kNegRows>(p, rel, samp_hi, c, negs, lane);
                 samp_hi += c;
             }
             // ring: stage the blocks up to slot m+2+w now — gather_list(m+2), one iteration on,
             // reads up to there after this group completes; the oldest slot still read, m+1-w,
-            // stays within kKRing of the newest (window <= 32)
+            // stays within KR of the newest staged slot (<= m+w+17; 2w + 19 <= KR)
             if (kring_on)
-                for (; 32 * kb_hi < nk && 32 * kb_hi <= m + 2 + window; ++kb_hi) stage_block(kb_hi);
+                for (; kKBlock * kb_hi < nk && kKBlock * kb_hi <= m + 2 + window; ++kb_hi) stage_block(kb_hi);
             cp_async_commit();
             cp_async_wait_but_last();
             __syncwarp();
@@ -561,9 +576,9 @@ size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, in
     const int TI = 32 / in->kp1;
     const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
     const int Lp = (L + 3) & ~3;
-    // long chunks: a kKRing-slot ring (window <= 32), else read from the batch stream in place
-    const int Lps = Lp <= kSmemChunk ? Lp : window <= 32 ? kKRing : 0;
-    const size_t ids = 16 + (size_t)(2 * Lps + 2 * R + kSampWinRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
+    // long chunks: a kring_slots(window)-slot ring (window <= 32), else read from the batch stream
+    const int Lps = Lp <= kSmemChunk ? Lp : window <= 32 ? kring_slots(window) : 0;
+    const size_t ids = 16 + (size_t)(2 * Lps + 2 * R + kNegRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 15) / 16 * 16;  // 16-B aligned slab (bulk copies); every byte counts
     if (slab_offset) *slab_offset = (int32_t)off;
     const size_t end = off + (size_t)(in->kp1 + 2 * window) * RS * 4;

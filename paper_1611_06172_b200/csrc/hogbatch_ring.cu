@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase);
     int32_t* nk_s = reinterpret_cast<int32_t*>(wbase + 8);
     const bool chunk_smem = p.Lp <= kRingSmemChunk;
-    int32_t* kid_s = reinterpret_cast<int32_t*>(wbase + 16);
+    // per-warp launch statistics live in shared memory (lane 0 updates them once per target):
+    // registers are the scarce resource at 11 warps per SM
+    unsigned long long* wst = reinterpret_cast<unsigned long long*>(wbase + 16);  // [6]
+    int32_t* kid_s = reinterpret_cast<int32_t*>(wbase + 64);
     const int Lps = chunk_smem ? p.Lp : 0;
     int32_t* negs = kid_s + 2 * Lps;                           // kRingNegRows x KS negatives ring
     float* gs = reinterpret_cast<float*>(negs + kRingNegRows * KS);  // G of the target, [tiles][32]
@@ -170,8 +173,8 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
 
     // per-warp counters of one launch; 32 bits where a launch (launch_words <= 2^31 raw words, one
     // unit in deterministic mode) cannot overflow them
-    unsigned st_words = 0, st_targets = 0, st_touch = 0;
-    unsigned long long st_pairs = 0, st_tail_pairs = 0, st_moved = 0;
+    enum { kWords, kTargets, kTouch, kPairs, kTailPairs, kMoved };
+    if (lane < 6) wst[lane] = 0;
     unsigned st_cold = 0;
     float st_loss_f = 0.f;
     double st_loss = 0.0, st_tail = 0.0;
@@ -205,11 +208,12 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
         cp_async_wait_all();
         __syncwarp();
         const int nk = *nk_s;
-        if (lane == 0) st_words += (unsigned)cnt;
+        if (lane == 0) wst[kWords] += (unsigned long long)cnt;
         if (nk < 2) continue;  // N = 0 for every kept target iff the chunk keeps < 2 words
 
         // ring state, in registers: lane s < S holds slot s (word id, reference count); lane
-        // r < S holds the slot of the position q in the window with q % S == r
+        // r holds the slot of the window position q with q & 31 == r (the window spans 2w+1 <= 31
+        // positions, so the low five bits are unique in it; no division by S)
         int32_t slot_word = -1, slot_ref = 0, pos_slot = 0;
         uint32_t freem = (S >= 32) ? kFull : ((1u << S) - 1u);
         int next_in = 0;  // next kept position to enter
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                     if (lane == sl) slot_word = id;
                 }
                 if (lane == sl) slot_ref += 1;
-                if (lane == next_in % S) pos_slot = sl;
+                if (lane == (next_in & 31)) pos_slot = sl;
             }
             // ---------------- a3: gather new ring rows + the K+1 output rows (one bulk copy each)
             const int nnew = __popc(newm);
@@ -273,15 +277,14 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
             }
             cp_async_commit();
             // lane i < N: context i = kept position lo + i (+1 past m), its slot and word
-            int my_cs = 0, my_ctx = -1;
+            int my_cs = 0;
             {
                 const int qpos = lo + lane + (lo + lane >= m ? 1 : 0);
-                const int src = (lane < N ? qpos : 0) % S;
+                const int src = (lane < N ? qpos : 0) & 31;
                 const int cs = __shfl_sync(kFull, pos_slot, src);
                 if (lane < N) {
                     my_cs = cs;
-                    my_ctx = kid[qpos];
-                    st_cold += my_ctx >= p.cold_from;
+                    st_cold += kid[qpos] >= p.cold_from;
                 }
             }
             const int64_t pi = (int64_t)p.epoch * p.n_local + (pp - p.shard_start);
@@ -454,7 +457,7 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                 const int q_lo = m - w < 0 ? 0 : m - w;
                 const int q_hi = (m == nk - 1) ? nk - 1 : m - w;
                 for (int q = q_lo; q <= q_hi; ++q) {
-                    const int sl = __shfl_sync(kFull, pos_slot, q % S);
+                    const int sl = __shfl_sync(kFull, pos_slot, q & 31);
                     int left = 0;
                     if (lane == sl) {
                         slot_ref -= 1;
@@ -503,19 +506,19 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
             st_loss += (double)st_loss_f;
             if (pp >= p.loss_tail_from) {
                 st_tail += (double)st_loss_f;
-                if (lane == 0) st_tail_pairs += (unsigned long long)(N * KP1);
+                if (lane == 0) wst[kTailPairs] += (unsigned long long)(N * KP1);
             }
             st_loss_f = 0.f;
             if (lane == 0) {
-                st_targets += 1;
-                st_touch += (unsigned)(N + KP1);
-                st_pairs += (unsigned long long)(N * KP1);
-                st_moved += (unsigned long long)(2 * KP1 + nnew + __popc(outm));
+                wst[kTargets] += 1;
+                wst[kTouch] += (unsigned long long)(N + KP1);
+                wst[kPairs] += (unsigned long long)(N * KP1);
+                wst[kMoved] += (unsigned long long)(2 * KP1 + nnew + __popc(outm));
             }
             if (p.dbg_len && pp >= p.dbg_base && pp < p.dbg_base + p.dbg_len) {
                 const int64_t qd = pp - p.dbg_base;
                 if (lane == 0) p.dbg_N[qd] = (uint8_t)N;
-                if (lane < N) p.dbg_ctx[qd * 2 * w + lane] = my_ctx;
+                if (lane < N) p.dbg_ctx[qd * 2 * w + lane] = kid[lo + lane + (lo + lane >= m ? 1 : 0)];
                 for (int k = lane; k < K; k += 32) p.dbg_neg[qd * K + k] = ng[k];
             }
             // the next target's gathers must see these reductions (R11) and the slab must be free
@@ -536,16 +539,16 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
         st_cold += __shfl_xor_sync(kFull, st_cold, o);
     }
     if (lane == 0) {
-        atomicAdd(&p.stats->words, (unsigned long long)st_words);
-        atomicAdd(&p.stats->targets, (unsigned long long)st_targets);
-        atomicAdd(&p.stats->row_touches, (unsigned long long)st_touch);
-        atomicAdd(&p.stats->loss_pairs, st_pairs);
+        atomicAdd(&p.stats->words, wst[kWords]);
+        atomicAdd(&p.stats->targets, wst[kTargets]);
+        atomicAdd(&p.stats->row_touches, wst[kTouch]);
+        atomicAdd(&p.stats->loss_pairs, wst[kPairs]);
         atomicAdd(&p.stats->loss_sum, st_loss);
         atomicAdd(&p.stats->row_touches_cold, (unsigned long long)st_cold);
-        atomicAdd(&p.stats->rows_moved, st_moved);
-        if (st_tail_pairs) {
+        atomicAdd(&p.stats->rows_moved, wst[kMoved]);
+        if (wst[kTailPairs]) {
             atomicAdd(&p.stats->loss_tail_sum, st_tail);
-            atomicAdd(&p.stats->loss_tail_pairs, st_tail_pairs);
+            atomicAdd(&p.stats->loss_tail_pairs, wst[kTailPairs]);
         }
     }
     // every warp of the CTA is done with TMEM before warp 0 frees it
@@ -590,8 +593,8 @@ const Inst* pick(int D, int K) {
 }  // namespace
 
 size_t ring_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
-    // [mbarrier 8 | nk 4 | pad][kid Lp][kinfo Lp][negs 8 x max(K,1)][G tiles x 32]
-    // [slab: KP1MAX B rows + (2w+1) ring rows, stride RS] — 20,992 B at cfg3: 11 units per SM
+    // [mbarrier 8 | nk 4 | pad 4 | stats 6 x 8 B][kid Lp][kinfo Lp][negs 8 x max(K,1)][G tiles x 32]
+    // [slab: KP1MAX B rows + (2w+1) ring rows, stride RS] — 21,040 B at cfg3: 11 units per SM
     const Inst* in = pick(D, K);
     if (!in || window > 15) return 0;  // the ring's slot and position masks are one warp wide
     const int RS = in->rs > 0 ? in->rs : 64 * in->cp2;
@@ -599,7 +602,7 @@ size_t ring_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset) {
     const size_t gfl = (size_t)((2 * window + TI - 1) / TI) * 32;
     const int Lp = (L + 3) & ~3;
     const int Lps = Lp <= kRingSmemChunk ? Lp : 0;
-    const size_t ids = 16 + (size_t)(2 * Lps + kRingNegRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
+    const size_t ids = 64 + (size_t)(2 * Lps + kRingNegRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
     const size_t off = (ids + 15) / 16 * 16;
     if (slab_offset) *slab_offset = (int32_t)off;
     return off + (size_t)(in->kp1 + 2 * window + 1) * RS * 4;

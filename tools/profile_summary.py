@@ -40,7 +40,7 @@ def launches(csv_path):
 
 def main(tag, csv_path, rep, bench_log):
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    bench = json.loads(open(bench_log).read().strip().splitlines()[-1])
+    bench = json.loads([ln for ln in open(bench_log).read().splitlines() if ln.startswith("{")][-1])
     agg = launches(csv_path)
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(ROOT, "profiles", f"{tag}_launches.md"), "w") as f:

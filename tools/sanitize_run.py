@@ -4,9 +4,11 @@ synccheck, one tool per invocation):
 
   compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_run.py
 
-Covers: setup kernels, the batch kernel (HogBatch and Alg.1 negatives), the three step kernels
-in Hogwild and deterministic mode, Alg.1, the rowpath measurement mode, the overlapped batch
-stream, the on-device input generator, and the 1-rank data-parallel path with C14/C15 sync.
+Covers: setup kernels, the batch kernel (HogBatch and Alg.1 negatives), the four step kernels
+(rows, window, window warp-specialised, ring with TMEM originals) in Hogwild and deterministic
+mode, the conflict-ticketed mode 2, Alg.1, the rowpath measurement mode, the overlapped batch
+stream, the long-chunk kept-list ring (cfg4 shape), the on-device input generator, and the
+1-rank data-parallel path with C13/C14/C15 sync.
 """
 import os
 import sys
@@ -44,6 +46,8 @@ def main():
     ids1 = c1.corpus().tokens(0, 6000)
     c2 = inputs.CONFIGS[2]
     ids2 = c2.corpus().tokens(0, 6000)
+    c4 = inputs.CONFIGS[4]
+    ids4 = c4.corpus().tokens(0, 9000)   # L = 1000: long chunks (kept-list ring), window 8, K = 15
     gen = torch.empty(4096, dtype=torch.int32, device="cuda")
     c2.corpus().tokens_cuda(0, 4096, gen)
     inputs.CONFIGS[5].corpus().tokens_cuda(7_000_000_000, 4096, gen)
@@ -52,6 +56,10 @@ def main():
         (ids2, c2, {"mode": 0, "kernel": 1}), (ids2, c2, {"mode": 0, "kernel": 2}), (ids2, c2, {"mode": 0, "kernel": 3}),
         (ids2, c2, {"mode": 1, "kernel": 3}), (ids2, c2, {"mode": 0, "algorithm": 1}),
         (ids2, c2, {"mode": 0, "rowpath_only": 1}), (ids1, c1, {"mode": 0, "overlap_batch": 1, "launch_words": 1000}),
+        (ids2, c2, {"mode": 0, "kernel": 4}), (ids2, c2, {"mode": 1, "kernel": 4}),
+        (ids2, c2, {"mode": 1, "kernel": 4, "ring_writeback": 1}), (ids2, c2, {"mode": 0, "kernel": 4, "rowpath_only": 1}),
+        (ids1, c1, {"mode": 2}), (ids2, c2, {"mode": 2}),
+        (ids4, c4, {"mode": 0}), (ids4, c4, {"mode": 1}),
     ]
     for ids, cfg, opts in cases:
         st = run(ids, cfg, opts)
