@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 kid = kid_s;
                 kinfo = kid_s + KR;
                 kmask = KR - 1;
-                for (kb_hi = 0; kKBlock * kb_hi < p.Lp && kKBlock * kb_hi <= window + 1; ++kb_hi) stage_block(kb_hi);
+                for (kb_hi = 0; kKBlock * kb_hi < p.Lp && kKBlock * kb_hi <= window + 3; ++kb_hi) stage_block(kb_hi);
             } else {
                 kid = kid_g;
                 kinfo = kinfo_g;
@@ -294,21 +294,23 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             // while the rows fly: fetch negatives ahead, build the next target's row list, alpha.
             // One cp.async group per target (possibly empty); targets fetched at iteration m' are
-            // >= m'+4 (a group of 4 when fewer than 4 remain ahead of m'+1), so waiting for all
-            // groups but this one covers target m+1, and the 8-target ring never overwrites one
-            // before gather_list has read it.
+            // >= m'+4 (a group of 4 when fewer than 4 remain ahead of m'+1), so waiting only for
+            // the groups at least 3 iterations old covers target m+1 without stalling on the
+            // fetch just issued, and the 8-target ring never overwrites one before gather_list
+            // has read it.
             if (K > 0 && samp_hi < nk && samp_hi - (m + 1) < kNegGrp) {
                 const int c = nk - samp_hi < kNegGrp ? nk - samp_hi : kNegGrp;
                 fetch_negs<kNegRows>(p, rel, samp_hi, c, negs, lane);
                 samp_hi += c;
             }
-            // ring: stage the blocks up to slot m+2+w now — gather_list(m+2), one iteration on,
-            // reads up to there after this group completes; the oldest slot still read, m+1-w,
-            // stays within KR of the newest staged slot (<= m+w+17; 2w + 19 <= KR)
+            // ring: stage the blocks up to slot m+4+w now — gather_list(m+4) reads up to there at
+            // iteration m+3, when this group is 3 iterations old and waited for; the oldest slot
+            // still read, m+1-w, stays within KR of the newest staged slot (<= m+w+19; KR >=
+            // 2w + 19). The chunk start stages up to w+3 (iterations 0-2) and waits for it.
             if (kring_on)
-                for (; kKBlock * kb_hi < nk && kKBlock * kb_hi <= m + 2 + window; ++kb_hi) stage_block(kb_hi);
+                for (; kKBlock * kb_hi < nk && kKBlock * kb_hi <= m + 4 + window; ++kb_hi) stage_block(kb_hi);
             cp_async_commit();
-            cp_async_wait_but_last();
+            cp_async_wait_but_3();
             __syncwarp();
             const int Nn = (m + 1 < nk) ? gather_list(m + 1, nk, rowid0 + (buf ^ 1) * RMAX) : 0;
             const int64_t pi = (int64_t)p.epoch * p.n_local + (pp - p.shard_start);

@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                 q_next = (qi + 1) * p.Q;
                 alpha = alpha_at(p, qi);
             }
-            cp_async_wait_but_last();
+            cp_async_wait_but_3();   // negatives are fetched >= 4 targets ahead
             mbar_wait(mbar, phase);
             phase ^= 1u;
             __syncwarp();

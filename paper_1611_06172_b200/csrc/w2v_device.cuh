@@ -65,6 +65,9 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // every cp.async group of this thread but the most recent one has completed
 __device__ __forceinline__ void cp_async_wait_but_last() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// every cp.async group but the three most recent ones has completed (groups issued >= 3
+// iterations ago: the step kernels stage their batch-stream reads that far ahead)
+__device__ __forceinline__ void cp_async_wait_but_3() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
 
 // ---- mbarrier + bulk (TMA engine, non-tensor) row copies --------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
