@@ -38,7 +38,10 @@ namespace w2v {
 namespace {
 
 constexpr int kRingSmemChunk = 256;  // chunks up to this many (padded) kept slots are staged in smem
-constexpr int kRingMaxWarps = 11;    // work units per CTA (one CTA per SM in Hogwild mode)
+#ifndef W2V_RING_WARPS
+#define W2V_RING_WARPS 11
+#endif
+constexpr int kRingMaxWarps = W2V_RING_WARPS;  // work units per CTA (one CTA per SM in Hogwild mode)
 constexpr int kRingNegRows = 8;      // ring of targets whose negatives are staged in smem
 constexpr int kRingNegGrp = 4;       // fetched 4 at a time, >= 3 targets ahead of use
 
@@ -378,8 +381,8 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                 // Σ_j G_ij B_j, in input order (M_in[ctx_i] += ΔIn_i, C10). When a word repeats
                 // inside the window two contexts share a slot, and a later input must still read
                 // the snapshot: then all ΔOut first, all slot updates second
-                const unsigned dupm = __match_any_sync(kFull, lane < N ? my_cs : -1 - lane);
-                const bool dup = __any_sync(kFull, lane < N && __popc(dupm) > 1);
+                // (conservative and cheap: some slot is shared by two window positions)
+                const bool dup = __any_sync(kFull, lane < S && slot_ref > 1);
                 auto delta_in = [&](int i, float2 (&din)[CP2]) {
                     float2 g2[KP1MAX];
 #pragma unroll
