@@ -69,3 +69,38 @@ def test_binding_fails_loudly_without_the_library(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_1611_06172_b200.binding"], capture_output=True,
                        text=True, env=env, cwd=ROOT, timeout=120)
     assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr
+
+
+def test_binding_rejects_wrong_dtypes_and_sizes(binding):
+    """The binding checks element type and size before the C-ABI sees a bare pointer (ADVICE r01:
+    an int64 corpus would be read as int32 pairs [id, 0, id, 0, ...], all valid ids)."""
+    import numpy as np
+    import torch
+    with pytest.raises(TypeError):
+        binding.train(np.arange(10, dtype=np.int64), 10, 1)
+    with pytest.raises(TypeError):
+        binding.train(torch.arange(10, dtype=torch.int64), 10, 1)
+    with pytest.raises(ValueError):
+        binding.train(np.arange(10, dtype=np.int32), 11, 1)          # n beyond the buffer
+    with pytest.raises(ValueError):
+        binding.train(np.arange(20, dtype=np.int32)[::2], 10, 1)     # not contiguous
+    with pytest.raises(TypeError):
+        binding.get_embeddings(0, np.zeros((4, 4), np.float64))
+    with pytest.raises(TypeError):
+        binding.set_embeddings(1, torch.zeros(4, 4, dtype=torch.float16))
+    with pytest.raises(TypeError):
+        binding.debug_batches(keep=np.zeros(4, np.int32))
+    with pytest.raises(TypeError):
+        binding.debug_alg1_negatives(np.zeros(4, np.int64))
+    # a well-typed call reaches the library (which then reports its own state error)
+    with pytest.raises(binding.W2VError) as e:
+        binding.train(np.arange(10, dtype=np.int32), 10, 1)
+    assert e.value.code == binding.ESTATE
+
+
+def test_error_codes_match_header(binding):
+    hdr = open(os.path.join(ROOT, "include", "w2v.h")).read()
+    codes = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define W2V_(E[A-Z]+|OK)\s+\(?(-?\d+)\)?", hdr)}
+    for name, val in codes.items():
+        assert getattr(binding, name) == val, name
+    assert codes["EPEER"] == -7
