@@ -333,12 +333,16 @@ def run_ours(args):
     ms_max, kern_max = maxr(ms, ms_step_kernel)
     value = n * args.steps / (ms_max / 1e3)
 
-    # e2e: the same call, every timed step, with a pinned HOST corpus (H2D inside) and the
-    # step's statistics (loss) read back to the host
+    # e2e: the same call, every timed step, with a pinned HOST corpus and the step's statistics
+    # (loss) read back to the host. Every step's corpus crosses PCIe inside the timed region:
+    # step 0's before it trains, step s+1's on the copy engine (w2v_prefetch) while step s trains
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(args.steps):
+    w2v.prefetch(host, n_local)
+    for s in range(args.steps):
+        if s + 1 < args.steps:
+            w2v.prefetch(host, n_local)
         w2v.train(host, n_local, 1)
         w2v.get_stats()
     f1.record(stream)
@@ -384,7 +388,9 @@ def run_ours(args):
             # per call the library reads back its setup info (32 B) before training and its
             # statistics (72 B) + finite-check flag block (32 B) after it
             "e2e": {"value": e2e_value, "unit": "words/s", "h2d_bytes_per_step": n_local * 4,
-                    "d2h_bytes_per_step": 32 + 72 + 32, "steps": args.steps},
+                    "d2h_bytes_per_step": 32 + 72 + 32, "steps": args.steps,
+                    "h2d": "pinned host corpus; step 0 copied before it trains, step s+1 copied on the copy "
+                           "engine (w2v_prefetch) while step s trains"},
             "gpu_launches": int(sum(s["launches"] for s in steps)),
             "clocks": clk.summary(),
         }

@@ -165,6 +165,15 @@ int w2v_set_stream(void* cuda_stream);
  * chunk-aligned per C13), ESTATE, ENOMEM, ECUDA, ENCCL. */
 int w2v_train(const int32_t* corpus_ids, int64_t n_tokens, int32_t epochs);
 
+/* Start copying a HOST corpus (int32[n_tokens], ideally pinned) to the device on the library's
+ * copy stream and return at once; a later w2v_train with the same pointer and n_tokens trains on
+ * that copy instead of copying again (the oldest matching prefetch first). Lets a caller overlap
+ * the next corpus's host->device transfer with the current w2v_train (plumbing around the step,
+ * the corpus arrives from the host). The host data must not change until the
+ * consuming w2v_train returns. At most two prefetches may be pending. Errors: ESTATE (before
+ * w2v_init, or two pending), EINVAL (NULL with n > 0, a device pointer), ENOMEM, ECUDA. */
+int w2v_prefetch(const int32_t* corpus_ids, int64_t n_tokens);
+
 /* Collective (all ranks must call): replace M_in and M_out by their elementwise mean over
  * ranks (R13). World 1: no-op. */
 int w2v_sync(void);

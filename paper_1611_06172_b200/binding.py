@@ -43,6 +43,7 @@ _lib.w2v_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int64]
 _lib.w2v_set_stream.argtypes = [_vp]
 _lib.w2v_train.argtypes = [_vp, ctypes.c_int64, ctypes.c_int32]
 _lib.w2v_sync.argtypes = []
+_lib.w2v_prefetch.argtypes = [_vp, ctypes.c_int64]
 _lib.w2v_get_embeddings.argtypes = [ctypes.c_int32, _vp]
 _lib.w2v_set_embeddings.argtypes = [ctypes.c_int32, _vp]
 _lib.w2v_get_stats.argtypes = [ctypes.POINTER(Stats)]
@@ -125,6 +126,12 @@ def set_stream(stream_handle):
 def train(corpus_ids, n_tokens=None, epochs=1):
     n = _numel(corpus_ids) if n_tokens is None else int(n_tokens)
     return _check(_lib.w2v_train(_checked(corpus_ids, "int32", n, "train corpus_ids"), n, epochs))
+
+
+def prefetch(corpus_ids, n_tokens=None):
+    """w2v_prefetch: start the host->device copy of a host corpus on the copy stream."""
+    n = _numel(corpus_ids) if n_tokens is None else int(n_tokens)
+    return _check(_lib.w2v_prefetch(_checked(corpus_ids, "int32", n, "prefetch corpus_ids"), n))
 
 
 def sync():

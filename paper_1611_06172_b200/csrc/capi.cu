@@ -89,6 +89,19 @@ struct Ctx {
     int sync_overlap = 0;        // C15: average in flight during the next interval (one late)
     float *syS = nullptr, *syC = nullptr;  // C15: average (S) of the snapshot (C), out of place
     cudaStream_t comm_stream = nullptr;
+    // w2v_prefetch: up to two host corpora copied ahead on the copy stream into their own device
+    // buffers; a w2v_train on the same host pointer and size consumes the oldest (FIFO)
+    cudaStream_t copy_stream = nullptr;
+    struct Prefetch {
+        const void* host = nullptr;
+        int64_t n = 0;
+        uint64_t seq = 0;
+        bool pending = false;
+        int32_t* buf = nullptr;
+        size_t cap = 0;
+        cudaEvent_t done = nullptr;
+    } pf[2];
+    uint64_t pf_seq = 0;
     int64_t Q = 10000;
     int allow_tn = 0;
     int64_t dbg_base = 0, dbg_len = 0;
@@ -336,6 +349,8 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
     CU(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&g.comm_stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&g.copy_stream, cudaStreamNonBlocking));
+    for (auto& f : g.pf) CU(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
     g.stream = g.own_stream;
     int rc;
     if ((rc = dmalloc((void**)&g.M, (size_t)V * 2 * g.Ds * sizeof(float), "the model [M_in|M_out]"))) return rc;
@@ -422,17 +437,29 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     CU(cudaEventRecord(ev0, st));
     // ---- corpus placement
     const int32_t* ids = ids_in;
+    int local_fail = 0;  // a rank-local failure before the first collective (reported through it)
     if (n > 0 && !is_device_ptr(ids_in)) {
-        if ((size_t)n > g.corpus_cap) {
-            cudaFree(g.corpus);
-            g.corpus = nullptr;
-            g.corpus_cap = 0;
-            int rc = dmalloc((void**)&g.corpus, (size_t)n * 4, "the device copy of a host corpus");
-            if (rc) return rc;
-            g.corpus_cap = (size_t)n;
+        Ctx::Prefetch* hit = nullptr;  // the oldest pending prefetch of this corpus (w2v_prefetch)
+        for (auto& f : g.pf)
+            if (f.pending && f.host == (const void*)ids_in && f.n == n && (!hit || f.seq < hit->seq)) hit = &f;
+        if (hit) {   // its H2D copy ran on the copy stream, overlapped with earlier work
+            CU(cudaStreamWaitEvent(st, hit->done, 0));
+            hit->pending = false;
+            ids = hit->buf;
+        } else {
+            if ((size_t)n > g.corpus_cap) {
+                cudaFree(g.corpus);
+                g.corpus = nullptr;
+                g.corpus_cap = 0;
+                local_fail = dmalloc((void**)&g.corpus, (size_t)n * 4, "the device copy of a host corpus");
+                if (local_fail && !dp()) return local_fail;
+                if (!local_fail) g.corpus_cap = (size_t)n;
+            }
+            if (!local_fail) {
+                CU(cudaMemcpyAsync(g.corpus, ids_in, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+                ids = g.corpus;
+            }
         }
-        CU(cudaMemcpyAsync(g.corpus, ids_in, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-        ids = g.corpus;
     }
     CU(cudaEventRecord(ev_h2d, st));
     // ---- a0: shard geometry (C13), counts, thresholds, sampler
@@ -441,11 +468,14 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     if (dp()) {
         if (!g.dp_tmp) { int rc = dmalloc((void**)&g.dp_tmp, (size_t)g.world * 8, "dp scratch"); if (rc) return rc; }
         std::vector<int64_t> h(g.world, 0);
-        h[g.rank] = n;
+        h[g.rank] = local_fail ? -1 : n;   // -1: this rank failed before the collectives
         CU(cudaMemcpyAsync(g.dp_tmp, h.data(), (size_t)g.world * 8, cudaMemcpyHostToDevice, st));
         NC(g_nccl.allReduce(g.dp_tmp, g.dp_tmp, (size_t)g.world, ncclInt64, ncclSum, g.comm, st));
         CU(cudaMemcpyAsync(h.data(), g.dp_tmp, (size_t)g.world * 8, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
+        if (local_fail) return local_fail;
+        for (int q = 0; q < g.world; ++q)
+            if (h[q] < 0) return fail(W2V_EPEER, "w2v_train: rank %d failed to place its corpus; nothing trained", q);
         n_global = 0;
         for (int q = 0; q < g.world; ++q) { if (q < g.rank) shard_start += h[q]; n_global += h[q]; }
         if (n_global == 0) return W2V_OK;
@@ -826,6 +856,33 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     return W2V_OK;
 }
 
+int w2v_prefetch(const int32_t* ids, int64_t n) {
+    NvtxRange nvtx("w2v_prefetch");
+    if (!g.live) return fail(W2V_ESTATE, "w2v_prefetch before w2v_init");
+    if (n < 0 || (!ids && n > 0)) return fail(W2V_EINVAL, "w2v_prefetch: bad corpus");
+    if (n == 0) return W2V_OK;
+    if (is_device_ptr(ids)) return fail(W2V_EINVAL, "w2v_prefetch: the corpus is already on the device");
+    Ctx::Prefetch* f = !g.pf[0].pending ? &g.pf[0] : !g.pf[1].pending ? &g.pf[1] : nullptr;
+    if (!f) return fail(W2V_ESTATE, "w2v_prefetch: two prefetched corpora are already pending (train on them first)");
+    if ((size_t)n > f->cap) {
+        cudaFree(f->buf);
+        f->buf = nullptr;
+        f->cap = 0;
+        int rc = dmalloc((void**)&f->buf, (size_t)n * 4, "a prefetched corpus");
+        if (rc) return rc;
+        f->cap = (size_t)n;
+    }
+    // the copy engine moves it while the compute stream trains on the previous corpus; the
+    // buffer is free: w2v_train is synchronous and consumed this slot's last corpus already
+    CU(cudaMemcpyAsync(f->buf, ids, (size_t)n * 4, cudaMemcpyHostToDevice, g.copy_stream));
+    CU(cudaEventRecord(f->done, g.copy_stream));
+    f->host = ids;
+    f->n = n;
+    f->seq = ++g.pf_seq;
+    f->pending = true;
+    return W2V_OK;
+}
+
 int w2v_sync(void) {
     NvtxRange nvtx_sync("w2v_sync");
     if (!g.live) return fail(W2V_ESTATE, "w2v_sync before w2v_init");
@@ -904,6 +961,10 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);
     NC(g_nccl.commInitRank(&g.comm, world, uid, rank));
+    if (!g.dp_tmp) {  // scratch of the consensus collectives, allocated here so w2v_train cannot fail on it
+        int rc = dmalloc((void**)&g.dp_tmp, (size_t)world * 8, "dp scratch");
+        if (rc) return rc;
+    }
     if (world > 1 && g.Ds != g.D) {
         // every model average moves 2*V*Ds floats: drop the 128-B row padding (worth ~0.7% on
         // one GPU) so the all-reduce sends exactly the 2*V*D model floats
@@ -948,8 +1009,14 @@ int w2v_finalize(void) {
     cudaFree(g.tick); cudaFree(g.turn);
     cudaStreamSynchronize(g.side);
     cudaStreamSynchronize(g.comm_stream);
+    cudaStreamSynchronize(g.copy_stream);
     cudaStreamDestroy(g.side);
     cudaStreamDestroy(g.comm_stream);
+    cudaStreamDestroy(g.copy_stream);
+    for (auto& f : g.pf) {
+        cudaFree(f.buf);
+        if (f.done) cudaEventDestroy(f.done);
+    }
     cudaFree(g.syS); cudaFree(g.syC);
     cudaStreamDestroy(g.own_stream);
     Ctx fresh;

@@ -604,6 +604,36 @@ def test_checkpoint_resume_is_exact(w2v):
     assert rel_l2(rest["M_in"], o_in) <= 1e-5 and rel_l2(rest["M_out"], o_out) <= 1e-5
 
 
+def test_prefetch_host_corpus(w2v):
+    """w2v_prefetch (the corpus's H2D copy on the copy stream, overlapped with other work): a
+    w2v_train on the prefetched host corpus is bit-identical to training on the device copy;
+    two prefetches are consumed in FIFO order by two trains; a third pending one is refused
+    (ESTATE), a device pointer is refused (EINVAL)."""
+    cfg = inputs.CONFIGS[1]
+    ids = cfg.corpus().tokens(0, 6000)
+    ref = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, epochs=1)
+    w2v.finalize()
+    host = torch.from_numpy(ids.copy()).pin_memory()
+    w2v.init(cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed)
+    w2v.set_option("mode", 1)
+    w2v.set_option("sentence_len", cfg.L)
+    w2v.prefetch(host, ids.size)
+    w2v.prefetch(host, ids.size)
+    with pytest.raises(w2v.W2VError) as e:
+        w2v.prefetch(host, ids.size)
+    assert e.value.code == w2v.ESTATE
+    with pytest.raises(w2v.W2VError) as e:
+        w2v.prefetch(host.cuda(), ids.size)
+    assert e.value.code == w2v.EINVAL
+    w2v.train(host, ids.size, 1)
+    M_in = np.empty((cfg.V, cfg.D), np.float32); w2v.get_embeddings(0, M_in)
+    assert np.array_equal(M_in, ref["M_in"])
+    w2v.train(host, ids.size, 1)           # consumes the second prefetch: a second epoch-0 pass
+    w2v.prefetch(host, ids.size)           # a slot is free again
+    st = w2v.get_stats()
+    assert st["words"] == 2 * ids.size
+
+
 def test_caller_stream_same_results(w2v):
     """w2v_set_stream (the bench hands the library torch's current stream): work enqueued on a
     caller's stream gives bit-identical deterministic results to the library's private stream."""
