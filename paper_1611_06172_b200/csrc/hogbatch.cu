@@ -60,23 +60,23 @@ __device__ __forceinline__ void red_release_add_u32(uint32_t* a, uint32_t v) {
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 constexpr int kSmemChunk = 256;  // chunks up to this many (padded) kept slots are staged in smem
-// long chunks: ring of kept slots (ids, offsets) in smem; it must span the 2w + 34 slots in use
-// (w+1 behind the reader, the staged block ahead): 64 for window <= 15, else 128 (window <= 32)
-// Staged 16 slots at a time; slots read at iteration m span [m+1-w, block end of m+2+w]:
-// 2w + 18 at most -> the smallest power of two >= 2w + 19 (32 at cfg5's window 5: a unit keeps
-// its 20.2 KB and 11 units fit per SM).
-constexpr int kKBlock = 16;
+// long chunks: ring of kept slots (ids, offsets) in smem, staged kKBlock = 8 slots at a time up to
+// slot m+4+w at iteration m; the slots still read after that span [m+1-w, m+w+11], so the ring
+// needs >= 2w + 11 slots: 32 up to window 10 (cfg4's window 8: 512 B less per unit than a
+// 64-slot ring, which is what lets a 12th unit fit at D = 128), 64 up to 26, 128 up to 32.
+constexpr int kKBlock = 8;
 // negatives of the next targets, staged by cp.async: a ring of 8 targets refilled 4 at a time
 // (load_chunk brings the first 8), so a target's group is >= 3 iterations old when it is read
 constexpr int kNegRows = 8;
 constexpr int kNegGrp = 4;
 __host__ __device__ constexpr int kring_slots(int window) {
-    return 2 * window + 19 <= 32 ? 32 : 2 * window + 19 <= 64 ? 64 : 128;
+    return 2 * window + 11 <= 32 ? 32 : 2 * window + 11 <= 64 ? 64 : 128;
 }
 
 #ifndef W2V_MINB
-#define W2V_MINB 11  // resident 1-warp CTAs per SM the register budget is sized for (the packed
-                     // D=300 slab lets 11 fit in smem; the padded ones 10)
+#define W2V_MINB 12  // resident 1-warp CTAs per SM the register budget is sized for: 168 registers
+                     // (3 warps per SM sub-partition) whether 11 or 12 fit; smem decides (D=300:
+                     // 11; cfg4's D=128: 12)
 #endif
 
 // CP2 = float2 columns per lane (lane owns d = 2*(lane + 32*c2) + {0,1}, D <= 64*CP2);
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     // kSmemChunk) are read in place from the batch stream (global, generic loads), which keeps a
     // unit's smem at the slab's size — at L = 1000 that is 8 KB, i.e. 3 more units per SM
     const bool chunk_smem = p.Lp <= kSmemChunk;
-    // long chunks with window <= 32: a ring of kring_slots kept slots (ids and offsets), staged 16
+    // long chunks with window <= 32: a ring of kring_slots kept slots (ids and offsets), staged 8
     // slots at a time by cp.async ahead of the targets that read them (an L2 round trip per
     // slot on the critical path otherwise: DESIGN.md §8, cfg4)
     const bool kring_on = !chunk_smem && window <= 32;
@@ -138,11 +138,11 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     const int32_t* kid_g = nullptr;    // the chunk's kept list in the batch stream (global)
     const int32_t* kinfo_g = nullptr;
     int kb_hi = 0;                 // ring: 32-slot blocks staged so far
-    auto stage_block = [&](int blk) {  // ring: slots [16 blk, 16 blk + 16) of ids and offsets
-        const int q = kKBlock * blk + 4 * (lane & 3);
-        if (lane < 8 && q < p.Lp) {
-            const int32_t* src = (lane < 4 ? kid_g : kinfo_g) + q;
-            cp_async16(kid_s + (lane < 4 ? 0 : KR) + (q & (KR - 1)), src);
+    auto stage_block = [&](int blk) {  // ring: slots [8 blk, 8 blk + 8) of ids and offsets
+        const int q = kKBlock * blk + 4 * (lane & 1);
+        if (lane < 4 && q < p.Lp) {
+            const int32_t* src = (lane < 2 ? kid_g : kinfo_g) + q;
+            cp_async16(kid_s + (lane < 2 ? 0 : KR) + (q & (KR - 1)), src);
         }
     };
     auto gather_list = [&](int m, int nk, int32_t* rowid) -> int {
@@ -305,8 +305,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             // ring: stage the blocks up to slot m+4+w now — gather_list(m+4) reads up to there at
             // iteration m+3, when this group is 3 iterations old and waited for; the oldest slot
-            // still read, m+1-w, stays within KR of the newest staged slot (<= m+w+19; KR >=
-            // 2w + 19). The chunk start stages up to w+3 (iterations 0-2) and waits for it.
+            // still read, m+1-w, stays within KR of the newest staged slot (<= m+w+11; KR >=
+            // 2w + 11). The chunk start stages up to w+3 (iterations 0-2) and waits for it.
             if (kring_on)
                 for (; kKBlock * kb_hi < nk && kKBlock * kb_hi <= m + 4 + window; ++kb_hi) stage_block(kb_hi);
             cp_async_commit();
