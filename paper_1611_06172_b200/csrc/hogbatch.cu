@@ -110,6 +110,12 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     int32_t* negs = rowid0 + 2 * RMAX;                        // kNegRows x KS negatives ring
     float* gs = reinterpret_cast<float*>(negs + kNegRows * KS);  // G of the target, [N][KP1MAX]
     constexpr int RS = RSC > 0 ? RSC : 64 * CP2;             // smem row stride (floats)
+    // wide output tiles finish their dots through a transpose in the B slab (see a4); it needs
+    // 32 x 36 floats of it
+#ifndef W2V_TRANSPOSE_DOTS
+#define W2V_TRANSPOSE_DOTS 1
+#endif
+    constexpr bool kTransposeDots = W2V_TRANSPOSE_DOTS && KP1MAX >= 16 && KP1MAX * RS >= 32 * 36;
     const bool lastok = RS >= 64 * CP2 || 2 * lane + 64 * (CP2 - 1) < D;  // lane's last float2 column exists
     float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
     float* As = Bs + KP1MAX * RS;                             // 2*window rows: context
@@ -373,6 +379,25 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                 }
 #pragma unroll
                 for (int u = TI * KP1MAX; u < 32; ++u) v[u] = 0.f;
+                float dot;
+                if constexpr (kTransposeDots) {
+                    // many outputs per tile (K+1 >= 16: two inputs per tile, ~4.5 tiles per
+                    // target at cfg4): finish the 32 dots through a 32 x 36 transpose in the B
+                    // slab, whose rows are already in registers (bq) and are only rewritten with
+                    // ΔOut after a6 — 8 STS.128 + 32 LDS + 31 FADD instead of the butterfly's
+                    // 31 SHFL + 62 FSEL + 31 FADD. Lane l sums column l = dot l, as below.
+                    float* T = Bs;
+                    __syncwarp();  // the previous tile's column reads are done
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        *reinterpret_cast<float4*>(T + lane * 36 + 4 * k) =
+                            make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    __syncwarp();
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) acc[r & 3] += T[r * 36 + lane];
+                    dot = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                } else {
 #pragma unroll
                 for (int st = 0; st < 5; ++st) {
                     const int o = 16 >> st;
@@ -384,7 +409,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
                         v[u] = keep + __shfl_xor_sync(kFull, send, o);
                     }
                 }
-                const float dot = v[0];
+                dot = v[0];
+                }
                 const bool valid = tt < TI && i0 + tt < N && tj < KP1;
                 const float ex = expf(-fabsf(dot));
                 const float rc = __frcp_rn(1.0f + ex);
