@@ -112,10 +112,10 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     constexpr int RS = RSC > 0 ? RSC : 64 * CP2;             // smem row stride (floats)
     // wide output tiles finish their dots through a transpose in the B slab (see a4); it needs
     // 32 x 36 floats of it
-#ifndef W2V_TRANSPOSE_DOTS
-#define W2V_TRANSPOSE_DOTS 1
+#ifndef W2V_TRANSPOSE_MIN_KP1
+#define W2V_TRANSPOSE_MIN_KP1 16
 #endif
-    constexpr bool kTransposeDots = W2V_TRANSPOSE_DOTS && KP1MAX >= 16 && KP1MAX * RS >= 32 * 36;
+    constexpr bool kTransposeDots = KP1MAX >= W2V_TRANSPOSE_MIN_KP1 && KP1MAX * RS >= 32 * 36;
     const bool lastok = RS >= 64 * CP2 || 2 * lane + 64 * (CP2 - 1) < D;  // lane's last float2 column exists
     float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
     float* As = Bs + KP1MAX * RS;                             // 2*window rows: context

@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
     int32_t* negs = kid_s + 2 * Lps;                           // kRingNegRows x KS negatives ring
     float* gs = reinterpret_cast<float*>(negs + kRingNegRows * KS);  // G of the target, [tiles][32]
     constexpr int RS = RSC > 0 ? RSC : 64 * CP2;
+#ifndef W2V_TRANSPOSE_MIN_KP1
+#define W2V_TRANSPOSE_MIN_KP1 16
+#endif
+    constexpr bool kTransposeDots = KP1MAX >= W2V_TRANSPOSE_MIN_KP1 && KP1MAX * RS >= 32 * 36;
     const bool lastok = RS >= 64 * CP2 || 2 * lane + 64 * (CP2 - 1) < D;
     float* Bs = reinterpret_cast<float*>(wbase + p.slab_offset);  // KP1MAX rows: target, negatives
     float* Ring = Bs + KP1MAX * RS;                               // S slots of M_in rows
@@ -356,6 +360,20 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                     }
 #pragma unroll
                     for (int u = TI * KP1MAX; u < 32; ++u) v[u] = 0.f;
+                    float dot;
+                    if constexpr (kTransposeDots) {  // as hogbatch.cu: through the idle B slab
+                        float* T = Bs;
+                        __syncwarp();
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            *reinterpret_cast<float4*>(T + lane * 36 + 4 * k) =
+                                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                        __syncwarp();
+                        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int r = 0; r < 32; ++r) acc[r & 3] += T[r * 36 + lane];
+                        dot = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                    } else {
 #pragma unroll
                     for (int st = 0; st < 5; ++st) {
                         const int o = 16 >> st;
@@ -367,7 +385,8 @@ __global__ void __launch_bounds__(32 * kRingMaxWarps, 1) hogbatch_ring_kernel(co
                             v[u] = keep + __shfl_xor_sync(kFull, send, o);
                         }
                     }
-                    const float dot = v[0];
+                    dot = v[0];
+                    }
                     const bool valid = tt < TI && i0 + tt < N && tj < KP1;
                     const float ex = expf(-fabsf(dot));
                     const float rc = __frcp_rn(1.0f + ex);
