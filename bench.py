@@ -285,6 +285,7 @@ def run_ours(args):
     w2v.set_option("sync_cold_every", cold)
     ovl = int(args.sync_overlap > 0)
     w2v.set_option("sync_overlap", ovl)
+    w2v.set_option("sync_device", int(args.sync_device > 0))   # C17: must precede dist_init
     w2v.set_option("kernel", args.kernel)
     if args.scatter_wait >= 0:
         w2v.set_option("scatter_wait", args.scatter_wait)
@@ -384,7 +385,10 @@ def run_ours(args):
             "config": workload_config(args, world),
             "run": {"units_per_sm": last["units_per_sm"], "mode": "hogwild",
                     "kernel": {1: "rows", 2: "window", 3: "window-wg", 4: "alg1", 5: "ring"}.get(last["kernel"]),
-                    "step_launches_per_step": last["step_launches"]},
+                    "step_launches_per_step": last["step_launches"],
+                    "sync_path": {0: None, 1: "nccl allreduce (ncclAvg)",
+                                  2: "C17 device kernel, NVLink peer loads/stores",
+                                  3: "C17 device kernel, NVLS multimem"}.get(last["sync_path"])},
             # per call the library reads back its setup info (32 B) before training and its
             # statistics (72 B) + finite-check flag block (32 B) after it
             "e2e": {"value": e2e_value, "unit": "words/s", "h2d_bytes_per_step": n_local * 4,
@@ -475,6 +479,9 @@ def main():
     ap.add_argument("--sync-cold-every", type=int, default=1,
                     help="C14 cold rows averaged every this many intervals (1 = every interval: C13)")
     ap.add_argument("--sync-overlap", type=int, default=0, help="C15 overlapped averaging (1 = on)")
+    ap.add_argument("--sync-device", type=int, default=0,
+                    help="C17: each average as one kernel over NCCL symmetric memory (NVLS multimem when "
+                         "available, else NVLink loads/stores) instead of ncclAllReduce (1 = on)")
     ap.add_argument("--scatter-wait", type=int, default=-1,
                     help="1: each target waits for its reductions to complete (R11); 0: only until read "
                          "(Hogwild staleness inside a chunk); -1: library default")

@@ -69,6 +69,12 @@ typedef struct {
     int64_t bytes_moved;     /* row bytes the step kernel actually gathered + reduced in the last
                                 w2v_train: bytes_row for the per-target kernels; fewer for the ring
                                 kernel, which keeps M_in rows of the window on chip             */
+    int64_t sync_path;       /* how a9 averages: 0 no communicator, 1 NCCL all-reduce (ncclAvg),
+                                2 one kernel over NCCL's symmetric window with peer loads/stores,
+                                3 the same kernel through the NVSwitch multicast address (NVLS
+                                multimem.ld_reduce / multimem.st) — option "sync_device"       */
+    int64_t sync_floats_owned; /* sync_path 2/3: floats this rank reduced and broadcast since
+                                w2v_dist_init (its 1/W slice of every averaged range)           */
 } w2v_stats_t;
 
 /* Create the model (Alg.1 l.1 "Given model parameter Omega = {M_in, M_out}").
@@ -96,6 +102,14 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          are averaged after every interval (default 0 = all rows, i.e. C13)
  *  "sync_cold_every"       C14: rows [H,V) only after every this many intervals and after the
  *                          last interval of each epoch (>=1; default 1)
+ *  "sync_device"           C17 (default 0; set BEFORE w2v_dist_init): the model is
+ *                          placed in ncclMemAlloc memory registered as an NCCL symmetric window
+ *                          and every C13/C14 average runs as ONE kernel (sync_dev.cu): each rank
+ *                          reduces its 1/W slice — through the NVSwitch multicast address
+ *                          (multimem.ld_reduce / multimem.st, NVLS) when NCCL provides one, else
+ *                          by peer loads/stores over NVLink — between two device-side barriers.
+ *                          Needs NCCL >= 2.28 and all ranks in one NVLink domain (else ENCCL
+ *                          from w2v_dist_init). C15's in-flight average stays an NCCL call.
  *  "sync_overlap"          C15 (default 0): the rows due are snapshot and averaged
  *                          on a communication stream while the next interval trains; their
  *                          correction M += avg - snapshot is applied one interval late; the last

@@ -10,12 +10,27 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libw2v.so")
 BUILD = os.path.join(PKG, "build")
-SOURCES = ["setup.cu", "batch.cu", "hogbatch.cu", "hogbatch_ring.cu", "hogbatch_win.cu", "hogbatch_wg.cu", "alg1.cu", "sync.cu", "capi.cu"]
+SOURCES = ["setup.cu", "batch.cu", "hogbatch.cu", "hogbatch_ring.cu", "hogbatch_win.cu", "hogbatch_wg.cu", "alg1.cu", "sync.cu", "sync_dev.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # IEEE division/sqrt are required for the bit-exact contract (C2, C9): no fast-math.
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
          "-I", os.path.join(ROOT, "include")]
+
+
+def _nccl_include() -> str:
+    """The NCCL headers of the nvidia-nccl wheel torch loads at run time (2.28: the symmetric-memory
+    device API sync_dev.cu uses; /usr/include holds an older 2.27 without it)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        inc = os.path.join(d, "include")
+        if os.path.exists(os.path.join(inc, "nccl_device.h")):
+            return inc
+    raise RuntimeError("nvidia-nccl wheel headers (nccl_device.h, NCCL >= 2.28) not found")
+
+
+FLAGS += ["-I", _nccl_include()]
 
 
 def _stale() -> bool:

@@ -30,7 +30,8 @@ class Stats(ctypes.Structure):
                 ("ms_batch", ctypes.c_double), ("l2_window_bytes", ctypes.c_int64), ("l2_carve_bytes", ctypes.c_int64),
                 ("syncs_hot", ctypes.c_int64), ("units_per_sm", ctypes.c_int64),
                 ("row_touches_cold", ctypes.c_int64), ("cold_from_row", ctypes.c_int64),
-                ("bytes_moved", ctypes.c_int64)]
+                ("bytes_moved", ctypes.c_int64), ("sync_path", ctypes.c_int64),
+                ("sync_floats_owned", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

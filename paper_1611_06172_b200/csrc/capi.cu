@@ -88,6 +88,10 @@ struct Ctx {
     int64_t sync_cold_every = 1; // C14: the other rows every this many intervals (and the last)
     int sync_overlap = 0;        // C15: average in flight during the next interval (one late)
     float *syS = nullptr, *syC = nullptr;  // C15: average (S) of the snapshot (C), out of place
+    int sync_device = 0;         // C17: a9 as one kernel over NCCL's symmetric window (sync_dev.cu)
+    DevSync ds;                  // ... its window + device communicator (open after w2v_dist_init)
+    bool M_nccl = false;         // the model lives in ncclMemAlloc memory (freed by ncclMemFree)
+    unsigned long long* ds_owned = nullptr;  // floats this rank reduced in the C17 kernel (stats)
     cudaStream_t comm_stream = nullptr;
     // w2v_prefetch: up to two host corpora copied ahead on the copy stream into their own device
     // buffers; a w2v_train on the same host pointer and size consumes the oldest (FIFO)
@@ -286,13 +290,19 @@ bool dp() { return g.comm != nullptr; }
 
 // a9: replace rows [row_lo, row_hi) of both matrices (one contiguous range of the interleaved
 // model) by their mean over ranks
-int sync_models(int64_t row_lo = 0, int64_t row_hi = -1) {
+int sync_models(int64_t row_lo = 0, int64_t row_hi = -1, int* launches = nullptr) {
     if (!dp()) return W2V_OK;
     NvtxRange nvtx("a9 model average");
     if (row_hi < 0) row_hi = g.V;
     if (row_hi <= row_lo) return W2V_OK;
-    NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.Ds, g.M + (size_t)row_lo * 2 * g.Ds,
-                        (size_t)(row_hi - row_lo) * 2 * g.Ds, ncclFloat32, ncclAvg, g.comm, g.stream));
+    if (g.ds.devcomm) {  // C17: one kernel, in place over the symmetric window (sync_dev.cu)
+        CU(devsync_launch(g.ds, (size_t)row_lo * 2 * g.Ds, (size_t)(row_hi - row_lo) * 2 * g.Ds, g.ds_owned,
+                          g.stream));
+        if (launches) ++*launches;
+    } else {
+        NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.Ds, g.M + (size_t)row_lo * 2 * g.Ds,
+                            (size_t)(row_hi - row_lo) * 2 * g.Ds, ncclFloat32, ncclAvg, g.comm, g.stream));
+    }
     if (row_lo == 0 && row_hi == g.V) g.st.syncs += 1;
     else g.st.syncs_hot += 1;
     if (g_nccl.commGetAsyncError) {  // a peer that failed surfaces here instead of as a hang later
@@ -382,6 +392,11 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "sync_period_words") { if (v < 1) return fail(W2V_EINVAL, "sync_period_words must be >= 1"); g.sync_period = v; }
     else if (k == "sync_hot_rows") { if (v < 0) return fail(W2V_EINVAL, "sync_hot_rows must be >= 0"); g.sync_hot_rows = v; }
     else if (k == "sync_cold_every") { if (v < 1) return fail(W2V_EINVAL, "sync_cold_every must be >= 1"); g.sync_cold_every = v; }
+    else if (k == "sync_device") {
+        if (v != 0 && v != 1) return fail(W2V_EINVAL, "sync_device must be 0/1");
+        if (g.comm) return fail(W2V_ESTATE, "sync_device must be set before w2v_dist_init (it places the model in NCCL symmetric memory)");
+        g.sync_device = (int)v;
+    }
     else if (k == "sync_overlap") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "sync_overlap must be 0/1"); g.sync_overlap = (int)v; }
     else if (k == "lr_quantum") { if (v < 1) return fail(W2V_EINVAL, "lr_quantum must be >= 1"); g.Q = v; }
     else if (k == "allow_target_negative") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "allow_target_negative must be 0/1"); g.allow_tn = (int)v; }
@@ -781,7 +796,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 const int64_t H = (g.sync_hot_rows <= 0 || g.sync_hot_rows >= g.V) ? g.V : g.sync_hot_rows;
                 const bool full = H == g.V || g.sync_cold_every <= 1 || (k + 1) % g.sync_cold_every == 0 || k == J - 1;
                 if (!g.sync_overlap) {
-                    int rc = full ? sync_models() : sync_models(0, H);
+                    int rc = full ? sync_models(0, -1, &launches) : sync_models(0, H, &launches);
                     if (rc) return rc;
                 } else {
                     // C15: apply the average in flight (its correction), then put this interval's
@@ -793,7 +808,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                         pend_hi = 0;
                     }
                     if (k == J - 1) {
-                        int rc = sync_models();
+                        int rc = sync_models(0, -1, &launches);
                         if (rc) return rc;
                     } else {
                         const int64_t hi_r = full ? g.V : H;
@@ -821,7 +836,10 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     SetupInfo hend{};
     CU(cudaMemcpyAsync(&hs, g.dstats, sizeof hs, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(&hend, g.info, sizeof hend, cudaMemcpyDeviceToHost, st));
+    unsigned long long owned = 0;
+    if (g.ds_owned) CU(cudaMemcpyAsync(&owned, g.ds_owned, 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (g.ds_owned) g.st.sync_floats_owned = (int64_t)owned;
     step_phase_report();
     win_phase_report();
     wg_phase_report();
@@ -888,7 +906,10 @@ int w2v_sync(void) {
     if (!g.live) return fail(W2V_ESTATE, "w2v_sync before w2v_init");
     int rc = sync_models();
     if (rc) return rc;
+    unsigned long long owned = 0;
+    if (g.ds_owned) CU(cudaMemcpyAsync(&owned, g.ds_owned, 8, cudaMemcpyDeviceToHost, g.stream));
     CU(cudaStreamSynchronize(g.stream));
+    if (g.ds_owned) g.st.sync_floats_owned = (int64_t)owned;
     return W2V_OK;
 }
 
@@ -965,20 +986,49 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
         int rc = dmalloc((void**)&g.dp_tmp, (size_t)world * 8, "dp scratch");
         if (rc) return rc;
     }
-    if (world > 1 && g.Ds != g.D) {
-        // every model average moves 2*V*Ds floats: drop the 128-B row padding (worth ~0.7% on
-        // one GPU) so the all-reduce sends exactly the 2*V*D model floats
+    g.st.sync_path = 1;
+    // every model average moves 2*V*Ds floats: at world > 1 drop the 128-B row padding (worth
+    // ~0.7% on one GPU) so the average covers exactly the 2*V*D model floats; with
+    // sync_device (C17) the model moves into ncclMemAlloc memory (the symmetric window)
+    const bool repack = world > 1 && g.Ds != g.D;
+    if (repack || g.sync_device) {
+        const int32_t Dn = repack ? g.D : g.Ds;
+        const size_t bytes = (size_t)g.V * 2 * Dn * sizeof(float);
         float* M2 = nullptr;
-        int rc = dmalloc((void**)&M2, (size_t)g.V * 2 * g.D * sizeof(float), "the unpadded data-parallel model");
-        if (rc) return rc;
-        const size_t half = (size_t)g.D * 4;
-        for (int h = 0; h < 2; ++h)
-            CU(cudaMemcpy2DAsync(M2 + h * g.D, 2 * half, g.M + h * g.Ds, (size_t)2 * g.Ds * 4, half, (size_t)g.V,
-                                 cudaMemcpyDeviceToDevice, g.stream));
+        int rc;
+        if (g.sync_device) {
+            std::string e;
+            void* b = nullptr;
+            rc = devsync_alloc(bytes, &b, &e) ? fail(W2V_ENCCL, "%s", e.c_str()) : W2V_OK;
+            M2 = (float*)b;
+            if (!rc) rc = dmalloc((void**)&g.ds_owned, 8, "sync_device counter");
+        } else {
+            rc = dmalloc((void**)&M2, bytes, "the unpadded data-parallel model");
+        }
+        rc = dp_agree(rc, g.stream);  // a rank that cannot allocate must not leave peers in a collective
+        if (rc) {
+            if (g.sync_device) devsync_free(M2); else cudaFree(M2);
+            return rc;
+        }
+        if (repack) {
+            const size_t half = (size_t)g.D * 4;
+            for (int h = 0; h < 2; ++h)
+                CU(cudaMemcpy2DAsync(M2 + h * g.D, 2 * half, g.M + h * g.Ds, (size_t)2 * g.Ds * 4, half, (size_t)g.V,
+                                     cudaMemcpyDeviceToDevice, g.stream));
+        } else {
+            CU(cudaMemcpyAsync(M2, g.M, bytes, cudaMemcpyDeviceToDevice, g.stream));
+        }
+        if (g.ds_owned) CU(cudaMemsetAsync(g.ds_owned, 0, 8, g.stream));
         CU(cudaStreamSynchronize(g.stream));
-        cudaFree(g.M);
+        if (g.M_nccl) devsync_free(g.M); else cudaFree(g.M);
         g.M = M2;
-        g.Ds = g.D;
+        g.M_nccl = g.sync_device != 0;
+        g.Ds = Dn;
+        if (g.sync_device) {  // collective: window registration + device communicator
+            std::string e;
+            if (devsync_open(g.comm, g.M, bytes, world, 1, &g.ds, &e)) return fail(W2V_ENCCL, "%s", e.c_str());
+            g.st.sync_path = g.ds.multimem ? 3 : 2;
+        }
     }
     return W2V_OK;
 }
@@ -1001,10 +1051,13 @@ int64_t w2v_dist_plan(int64_t n_global, int32_t L, int32_t world, int32_t rank, 
 int w2v_finalize(void) {
     if (!g.live) return W2V_OK;
     cudaStreamSynchronize(g.stream);
+    devsync_close(&g.ds);
     if (g.comm) g_nccl.commDestroy(g.comm);
     free_dbg();
     free_bt();
-    cudaFree(g.M); cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
+    if (g.M_nccl) devsync_free(g.M); else cudaFree(g.M);
+    cudaFree(g.ds_owned);
+    cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
     cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
     cudaFree(g.tick); cudaFree(g.turn);
     cudaStreamSynchronize(g.side);

@@ -2,6 +2,9 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <string>
+
+struct ncclComm;
 
 namespace w2v {
 
@@ -108,6 +111,21 @@ void wg_phase_report();  // (experiment builds with W2V_PHASE_TIMING)
 // sync.cu (C15 overlapped averaging)
 cudaError_t launch_sync_apply(float* M, const float* S, const float* C, size_t n, int sms, cudaStream_t st);
 cudaError_t launch_sync_snap(const float* M, float* C, size_t n, int sms, cudaStream_t st);
+
+// sync_dev.cu: a9 as one kernel over NCCL's symmetric window (option "sync_device", C17)
+constexpr int kDevSyncCtas = 296;  // 2 per SM; also the LSA barrier count
+struct DevSync {
+    void* comm = nullptr;     // ncclComm_t
+    void* win = nullptr;      // ncclWindow_t of the model buffer
+    void* devcomm = nullptr;  // heap ncclDevComm
+    int multimem = 0;         // 1: NVLS multicast path, 0: LSA peer loads/stores
+    int lsa_size = 0;
+};
+int devsync_alloc(size_t bytes, void** buf, std::string* err);
+void devsync_free(void* buf);
+int devsync_open(ncclComm* comm, void* buf, size_t bytes, int world, int want_mm, DevSync* ds, std::string* err);
+void devsync_close(DevSync* ds);
+cudaError_t devsync_launch(const DevSync& ds, size_t off, size_t n, unsigned long long* counted, cudaStream_t st);
 
 // alg1.cu (Algorithm 1, the level-1 baseline)
 bool alg1_supported(int D, int K);

@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--hot", type=int, default=0)
     ap.add_argument("--cold-every", type=int, default=1)
     ap.add_argument("--overlap", type=int, default=0)
+    ap.add_argument("--sync-device", type=int, default=0)
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -54,6 +55,7 @@ def main():
     w2v.set_option("sync_hot_rows", a.hot)
     w2v.set_option("sync_cold_every", a.cold_every)
     w2v.set_option("sync_overlap", a.overlap)
+    w2v.set_option("sync_device", a.sync_device)   # C17: the average as one kernel (sync_dev.cu)
     uid = torch.zeros(128, dtype=torch.uint8)
     if rank == 0:
         uid.copy_(torch.frombuffer(bytearray(w2v.dist_unique_id()), dtype=torch.uint8))
@@ -84,7 +86,7 @@ def main():
     np.savez(os.path.join(a.out, f"gpu_r{rank}.npz"), M_in=g_in, M_out=g_out, o_in=o_in, o_out=o_out,
              words=st["words"], targets=st["targets"], row_touches=st["row_touches"], syncs=st["syncs"],
              syncs_hot=st["syncs_hot"], o_words=o_st["words"], o_targets=o_st["targets"],
-             o_row_touches=o_st["row_touches"], J=J)
+             o_row_touches=o_st["row_touches"], J=J, sync_path=st["sync_path"])
     dist.barrier()
     dist.destroy_process_group()
 

@@ -31,8 +31,9 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world", [1, 2])
-@pytest.mark.parametrize("hot,cold_every,overlap", [(0, 1, 0), (150, 3, 0), (0, 1, 1)])
-def test_replicas_match_oracle_protocol(tmp_path, world, hot, cold_every, overlap):
+@pytest.mark.parametrize("hot,cold_every,overlap,sync_device", [(0, 1, 0, 0), (150, 3, 0, 0), (0, 1, 1, 0),
+                                                               (0, 1, 0, 1), (150, 3, 0, 1)])
+def test_replicas_match_oracle_protocol(tmp_path, world, hot, cold_every, overlap, sync_device):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs (visible: {torch.cuda.device_count()})")
     import __graft_entry__
@@ -40,7 +41,7 @@ def test_replicas_match_oracle_protocol(tmp_path, world, hot, cold_every, overla
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(HERE, "dist_gpu_worker.py"), "--out", str(tmp_path), "--hot", str(hot),
-           "--cold-every", str(cold_every), "--overlap", str(overlap)]
+           "--cold-every", str(cold_every), "--overlap", str(overlap), "--sync-device", str(sync_device)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(os.path.join(tmp_path, f"gpu_r{k}.npz")) for k in range(world)]
@@ -49,6 +50,7 @@ def test_replicas_match_oracle_protocol(tmp_path, world, hot, cold_every, overla
             assert int(x[f]) == int(x["o_" + f]), (k, f)
         J = int(x["J"])
         assert int(x["syncs"]) + int(x["syncs_hot"]) == J  # one average per interval (C13/C14/C15)
+        assert int(x["sync_path"]) in ((2, 3) if sync_device else (1,))  # C17 kernel (LSA or NVLS) / NCCL
         for name, g, o in (("M_in", x["M_in"], x["o_in"]), ("M_out", x["M_out"], x["o_out"])):
             e, rr = rel_l2(g, o), row_rel_max(g, o)
             print(f"W={world} H={hot} C={cold_every} overlap={overlap} rank {k} {name}: rel L2 {e:.3e}, "

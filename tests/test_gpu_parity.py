@@ -490,13 +490,17 @@ def test_cfg4_full_size_sampled_stream(w2v):
 
 
 # ------------------------------------------------------------------ data-parallel path --------
-@pytest.mark.parametrize("hot_rows,cold_every,overlap", [(0, 1, 0), (100, 3, 0), (100, 3, 1), (0, 1, 1)])
-def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap):
+@pytest.mark.parametrize("hot_rows,cold_every,overlap,sync_device",
+                         [(0, 1, 0, 0), (100, 3, 0, 0), (100, 3, 1, 0), (0, 1, 1, 0),
+                          (0, 1, 0, 1), (100, 3, 0, 1), (0, 1, 1, 1)])
+def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap, sync_device):
     """The DP code path (C13: n_local all-gather, histogram all-reduce, sync intervals, model
     averaging via NCCL; C14: hot-prefix averaging with the cold rows every 3rd interval; C15: the
-    average in flight on the comm stream and applied one interval late) on a 1-rank communicator
-    must reproduce the plain run exactly (deterministic mode; mean of one replica = identity),
-    with the expected full and hot-only sync counts."""
+    average in flight on the comm stream and applied one interval late; C17: every average as one
+    kernel over NCCL's symmetric window, the model in ncclMemAlloc memory) on a 1-rank
+    communicator must reproduce the plain run exactly (deterministic mode; mean of one replica =
+    identity), with the expected full and hot-only sync counts — and, for C17, the kernel must
+    have reduced exactly the floats of every averaged range (its device-side count)."""
     cfg = inputs.CONFIGS[1]
     ids = cfg.corpus().tokens(0, cfg.n)
     plain = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L)
@@ -508,7 +512,10 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap):
     w2v.set_option("sync_hot_rows", hot_rows)
     w2v.set_option("sync_cold_every", cold_every)
     w2v.set_option("sync_overlap", overlap)
+    w2v.set_option("sync_device", sync_device)
     w2v.dist_init(0, 1, w2v.dist_unique_id())
+    with pytest.raises(w2v.W2VError, match="before w2v_dist_init"):
+        w2v.set_option("sync_device", sync_device)
     w2v.train(torch.from_numpy(ids).cuda(), ids.size, 1)
     M_in = np.empty((cfg.V, cfg.D), np.float32); M_out = np.empty_like(M_in)
     w2v.get_embeddings(0, M_in); w2v.get_embeddings(1, M_out)
@@ -519,9 +526,16 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap):
     assert st["syncs"] == full and st["syncs_hot"] == J - full
     assert (full < J) == (hot_rows > 0)
     assert np.array_equal(M_in, plain["M_in"]) and np.array_equal(M_out, plain["M_out"])
+    Ds = (cfg.D + 31) // 32 * 32   # the 1-rank model keeps its 128-B row padding
+    row = 2 * Ds
+    owned = cfg.V * row if overlap else full * cfg.V * row + (J - full) * hot_rows * row
+    assert st["sync_path"] == (2 if sync_device else 1)   # no multicast object on one GPU: LSA path
+    assert st["sync_floats_owned"] == (owned if sync_device else 0)
     w2v.sync()
     w2v.get_embeddings(0, M_in)
     assert np.array_equal(M_in, plain["M_in"])
+    if sync_device:
+        assert w2v.get_stats()["sync_floats_owned"] == owned + cfg.V * row
 
 
 def test_rowpath_only_measurement_mode(w2v):
