@@ -120,10 +120,12 @@ STAT_KERNEL = {1: 1, 2: 2, 3: 3, 4: 5}   # option "kernel" -> w2v_stats_t.kernel
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("n", [1000, 5000, 20000])
+@pytest.mark.parametrize("n", [2, 10, 100, 1000, 5000, 20000])
 def test_cfg1_deterministic_parity(w2v, n, kernel):
     """BASELINE cfg1 (V=1000, D=32, window=2, K=3, t=0, Zipf(1.0)): bit-exact batch stream and
-    <=1e-5 relative L2 of both matrices against the fp64 oracle after n raw tokens."""
+    <=1e-5 relative L2 of both matrices against the fp64 oracle after n raw tokens — with t=0
+    every token of a chunk is a target, so after k = n targets: SURVEY.md §8(c)'s k in
+    {1, 10, 100, 1000, all} (k=2 stands for 1: a lone token has no context)."""
     cfg = inputs.CONFIGS[1]
     ids = cfg.corpus().tokens(0, n)
     g = run_gpu(w2v, ids, cfg.V, cfg.D, cfg.window, cfg.K, cfg.alpha, cfg.t, cfg.seed, cfg.L, debug=(0, n),
