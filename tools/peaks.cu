@@ -29,8 +29,9 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 }
 
 // one warp = one unit: batches of R rows gathered then reduced, like one target of the step
+// (rows [0, n_store) of a batch are written back by a plain bulk store instead of the reduction)
 __global__ void rowpath_kernel(float* base, uint32_t nrows, uint32_t row_floats, uint32_t row_bytes, int R,
-                               int batches, int warp_bytes) {
+                               int batches, int warp_bytes, int n_store) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* wb = smem + (size_t)w * warp_bytes;
@@ -63,8 +64,13 @@ __global__ void rowpath_kernel(float* base, uint32_t nrows, uint32_t row_floats,
             "r"(phase)
             : "memory");
         phase ^= 1u;
-        if (lane < R)
+        if (lane < R && lane >= n_store)
             asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                             base + (size_t)id * row_floats),
+                         "r"(smem_u32(rows + (size_t)lane * row_floats)), "r"(row_bytes)
+                         : "memory");
+        if (lane < R && lane < n_store)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
                              base + (size_t)id * row_floats),
                          "r"(smem_u32(rows + (size_t)lane * row_floats)), "r"(row_bytes)
                          : "memory");
@@ -256,7 +262,14 @@ extern "C" {
 
 // row_bytes % 16 == 0; R rows per batch (<= 32); warps_per_sm resident 1-warp... units per SM.
 // Returns 0 and *gbs = (gathered + reduced row bytes) / s, or a CUDA error code.
+int peaks_l2_rowpath_store(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs);
 int peaks_l2_rowpath(int row_bytes, int R, int warps_per_sm, double* gbs) {
+    return peaks_l2_rowpath_store(row_bytes, R, warps_per_sm, 0, gbs);
+}
+
+// the same with the first n_store rows of every batch written back by a plain bulk store
+// (cp.async.bulk.global.shared::cta) instead of the fp32 reduce-add
+int peaks_l2_rowpath_store(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs) {
     if (row_bytes <= 0 || row_bytes % 16 || R < 1 || R > 32 || warps_per_sm < 1) return -1;
     const int sms = sm_count();
     const uint32_t row_floats = (uint32_t)((row_bytes + 127) / 128 * 32);   // 128-B row stride
@@ -275,7 +288,7 @@ int peaks_l2_rowpath(int row_bytes, int R, int warps_per_sm, double* gbs) {
     for (int pass = 0; pass < 2; ++pass) {
         cudaEventRecord(t.a);
         rowpath_kernel<<<sms * cpsm, 32 * wpc, smem>>>(base, nrows, row_floats, (uint32_t)row_bytes, R, batches,
-                                                       warp_bytes);
+                                                       warp_bytes, n_store);
         cudaEventRecord(t.b);
         cudaEventSynchronize(t.b);
         cudaEventElapsedTime(&ms, t.a, t.b);
