@@ -1026,7 +1026,17 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
         g.Ds = Dn;
         if (g.sync_device) {  // collective: window registration + device communicator
             std::string e;
-            if (devsync_open(g.comm, g.M, bytes, world, 1, &g.ds, &e)) return fail(W2V_ENCCL, "%s", e.c_str());
+            auto agree_min = [](int v) -> int {  // min over ranks (NCCL all-reduce on the scratch)
+                int64_t h = v;
+                if (cudaMemcpyAsync(g.dp_tmp, &h, 8, cudaMemcpyHostToDevice, g.stream) != cudaSuccess) return -1;
+                if (g_nccl.allReduce(g.dp_tmp, g.dp_tmp, 1, ncclInt64, ncclMin, g.comm, g.stream) != ncclSuccess)
+                    return -1;
+                if (cudaMemcpyAsync(&h, g.dp_tmp, 8, cudaMemcpyDeviceToHost, g.stream) != cudaSuccess) return -1;
+                if (cudaStreamSynchronize(g.stream) != cudaSuccess) return -1;
+                return (int)h;
+            };
+            if (devsync_open(g.comm, g.M, bytes, world, 1, +agree_min, &g.ds, &e))
+                return fail(W2V_ENCCL, "%s", e.c_str());
             g.st.sync_path = g.ds.multimem ? 3 : 2;
         }
     }

@@ -199,7 +199,11 @@ void devsync_free(void* buf) {
 
 // Collective over the communicator: register the model buffer as a symmetric window and create
 // the device communicator (NVLS multicast if NCCL can give it, else LSA loads/stores).
-int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_mm, DevSync* ds, std::string* err) {
+// agree_min(v): the minimum of v over all ranks (a collective supplied by the caller), so that a
+// multicast team that only some ranks could create is dropped on every rank (the fallback
+// creation is collective too and must be called by all or none)
+int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_mm, int (*agree_min)(int),
+                 DevSync* ds, std::string* err) {
     ncclWindow_t win = nullptr;
     ncclResult_t r = g_dev.winRegister(comm, buf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
     if (r != ncclSuccess) { set_err(err, "sync_device: ncclCommWindowRegister", r); return 1; }
@@ -208,9 +212,20 @@ int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_m
     std::memset(&req, 0, sizeof req);
     req.lsaBarrierCount = kDevSyncCtas;
     int mm = 0;
-    if (want_mm && world > 1) {
+    if (want_mm) {  // also at W = 1: exercises the failed-attempt fallback on one-GPU boxes
         req.lsaMultimem = true;
-        mm = g_dev.devCommCreate(comm, &req, dc) == ncclSuccess && dc->lsaMultimem.mcBasePtr != nullptr;
+        const bool made = g_dev.devCommCreate(comm, &req, dc) == ncclSuccess;
+        mm = made && dc->lsaMultimem.mcBasePtr != nullptr;
+        const int all = agree_min(mm);
+        if (all < 0) {
+            if (made) g_dev.devCommDestroy(comm, dc);
+            delete dc;
+            g_dev.winDeregister(comm, win);
+            *err = "sync_device: the multicast agreement collective failed";
+            return 1;
+        }
+        if (made && !all) g_dev.devCommDestroy(comm, dc);
+        mm = all;
         req.lsaMultimem = false;
     }
     if (!mm) {

@@ -123,7 +123,8 @@ struct DevSync {
 };
 int devsync_alloc(size_t bytes, void** buf, std::string* err);
 void devsync_free(void* buf);
-int devsync_open(ncclComm* comm, void* buf, size_t bytes, int world, int want_mm, DevSync* ds, std::string* err);
+int devsync_open(ncclComm* comm, void* buf, size_t bytes, int world, int want_mm, int (*agree_min)(int), DevSync* ds,
+                 std::string* err);
 void devsync_close(DevSync* ds);
 cudaError_t devsync_launch(const DevSync& ds, size_t off, size_t n, unsigned long long* counted, cudaStream_t st);
 

@@ -43,7 +43,7 @@ def main():
         st = w2v.get_stats()
         Ds = (a.D + 31) // 32 * 32
         model_bytes = a.V * 2 * Ds * 4
-        out["c16_kernel" if dev else "nccl_allreduce"] = {
+        out["c17_kernel" if dev else "nccl_allreduce"] = {
             "ms": ms, "sync_path": st["sync_path"], "model_bytes": model_bytes,
             "GBps_read_plus_write": 2 * model_bytes / ms / 1e6 if dev else None,
             "floats_owned": st["sync_floats_owned"]}
