@@ -234,6 +234,14 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]);
 int64_t w2v_dist_plan(int64_t n_global, int32_t L, int32_t world, int32_t rank,
                       int64_t sync_period_words, int64_t* out, int64_t max_out);
 
+/* Pure host (no device needed): the part of an averaged float range [off, off+n) of the model
+ * that rank `rank` of `world` reduces and broadcasts in the C17 device average (option
+ * "sync_device"; PAPER.md:154-157 periodic synchronisation, reading R13): out[0..3] = s0, a0, a1,
+ * s1 — its floats [s0, s1) = [off + n*rank/world, off + n*(rank+1)/world), a scalar head
+ * [s0, a0) up to the first 16-B aligned float, a float4 body [a0, a1), a scalar tail [a1, s1).
+ * The kernel uses exactly this arithmetic. EINVAL on negative sizes or rank outside [0, world). */
+int w2v_dist_sync_slice(int64_t off, int64_t n, int32_t world, int32_t rank, int64_t out[4]);
+
 /* Free everything (model, tables, buffers, NCCL communicator). Safe to call twice. */
 int w2v_finalize(void);
 

@@ -55,6 +55,8 @@ _lib.w2v_dist_init.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp]
 _lib.w2v_dist_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]
 _lib.w2v_dist_plan.restype = ctypes.c_int64
+_lib.w2v_dist_sync_slice.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.POINTER(ctypes.c_int64)]
 _lib.w2v_finalize.argtypes = []
 _lib.w2v_last_error.restype = ctypes.c_char_p
 
@@ -193,6 +195,13 @@ def dist_plan(n_global, L, world, rank, sync_period_words):
     out = (ctypes.c_int64 * (3 + 2 * cap))()
     J = _check(_lib.w2v_dist_plan(n_global, L, world, rank, sync_period_words, out, cap))
     return [(out[3 + 2 * k], out[4 + 2 * k]) for k in range(min(J, cap))]
+
+
+def dist_sync_slice(off, n, world, rank):
+    """(s0, a0, a1, s1): rank's floats of an averaged range in the C17 device average; pure host."""
+    out = (ctypes.c_int64 * 4)()
+    _check(_lib.w2v_dist_sync_slice(off, n, world, rank, out))
+    return tuple(out)
 
 
 def dist_shard(n_global, L, world, rank):

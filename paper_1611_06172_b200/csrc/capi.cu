@@ -1043,6 +1043,15 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
     return W2V_OK;
 }
 
+int w2v_dist_sync_slice(int64_t off, int64_t n, int32_t world, int32_t rank, int64_t out[4]) {
+    if (off < 0 || n < 0 || world < 1 || rank < 0 || rank >= world || !out)
+        return fail(W2V_EINVAL, "w2v_dist_sync_slice: bad arguments");
+    size_t s0, a0, a1, s1;
+    devsync_slice((size_t)off, (size_t)n, rank, world, &s0, &a0, &a1, &s1);
+    out[0] = (int64_t)s0; out[1] = (int64_t)a0; out[2] = (int64_t)a1; out[3] = (int64_t)s1;
+    return W2V_OK;
+}
+
 int64_t w2v_dist_plan(int64_t n_global, int32_t L, int32_t world, int32_t rank, int64_t P, int64_t* out,
                       int64_t max_out) {
     if (n_global < 0 || L < 1 || world < 1 || rank < 0 || rank >= world || P < 1 || !out)

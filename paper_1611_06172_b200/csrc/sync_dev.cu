@@ -100,9 +100,8 @@ __global__ void __launch_bounds__(kThreads, 2) avg_kernel(ncclWindow_t win, nccl
 
     const int W = dc.lsaSize, r = dc.lsaRank;
     const float inv = 1.0f / (float)W;
-    const size_t s0 = off + n * (size_t)r / (size_t)W, s1 = off + n * (size_t)(r + 1) / (size_t)W;
-    const size_t a0 = s0 + 3 < s1 ? (s0 + 3) & ~(size_t)3 : s1;  // first 16-B aligned float
-    const size_t a1 = a0 + ((s1 - a0) & ~(size_t)3);               // end of the float4 body
+    size_t s0, a0, a1, s1;
+    devsync_slice(off, n, r, W, &s0, &a0, &a1, &s1);
     const size_t T = (size_t)gridDim.x * kThreads, tid = (size_t)blockIdx.x * kThreads + threadIdx.x;
     uint32_t mine = 0;
 

@@ -114,6 +114,15 @@ cudaError_t launch_sync_snap(const float* M, float* C, size_t n, int sms, cudaSt
 
 // sync_dev.cu: a9 as one kernel over NCCL's symmetric window (option "sync_device", C17)
 constexpr int kDevSyncCtas = 296;  // 2 per SM; also the LSA barrier count
+// rank r of W owns floats [s0, s1) = [off + n*r/W, off + n*(r+1)/W) of an averaged range: a scalar
+// head [s0, a0) up to the first 16-B aligned float, a float4 body [a0, a1), a scalar tail [a1, s1)
+__host__ __device__ inline void devsync_slice(size_t off, size_t n, int r, int W, size_t* s0, size_t* a0, size_t* a1,
+                                              size_t* s1) {
+    *s0 = off + n * (size_t)r / (size_t)W;
+    *s1 = off + n * (size_t)(r + 1) / (size_t)W;
+    *a0 = *s0 + 3 < *s1 ? (*s0 + 3) & ~(size_t)3 : *s1;
+    *a1 = *a0 + ((*s1 - *a0) & ~(size_t)3);
+}
 struct DevSync {
     void* comm = nullptr;     // ncclComm_t
     void* win = nullptr;      // ncclWindow_t of the model buffer

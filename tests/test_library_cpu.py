@@ -104,3 +104,30 @@ def test_error_codes_match_header(binding):
     for name, val in codes.items():
         assert getattr(binding, name) == val, name
     assert codes["EPEER"] == -7
+
+
+def test_dist_sync_slices_tile_every_range(binding):
+    """C17 (sync_dev.cu): the W ranks' slices of an averaged range tile it exactly, in rank order,
+    balanced to one float, each split into a scalar head of < 4 floats up to a 16-B boundary, a
+    float4 body on 16-B boundaries and a scalar tail of < 4 floats — for the model ranges the
+    library averages (multiples of 2*Ds floats) and for arbitrary offsets and sizes."""
+    import random
+    rng = random.Random(7)
+    cases = [(0, 2 * 300 * 1_000_000, 8), (0, 2 * 320 * 1_000, 1), (2 * 300 * 5000, 2 * 300 * 45_000, 3),
+             (0, 0, 4), (0, 3, 8), (5, 7, 2), (1, 1, 1)]
+    cases += [(rng.randrange(0, 1 << 20), rng.randrange(0, 1 << 22), rng.randrange(1, 9)) for _ in range(300)]
+    for off, n, W in cases:
+        prev = off
+        sizes = []
+        for r in range(W):
+            s0, a0, a1, s1 = binding.dist_sync_slice(off, n, W, r)
+            assert s0 == prev and s0 <= a0 <= a1 <= s1, (off, n, W, r)
+            assert (a1 - a0) % 4 == 0 and (a0 % 4 == 0 or a0 == s1)
+            assert a0 - s0 < 4 and (s1 - a1 < 4), (off, n, W, r, s0, a0, a1, s1)
+            if a1 > a0:
+                assert a0 % 4 == 0
+            sizes.append(s1 - s0)
+            prev = s1
+        assert prev == off + n and max(sizes) - min(sizes) <= 1
+    with pytest.raises(binding.W2VError):
+        binding.dist_sync_slice(0, 10, 2, 2)
