@@ -52,7 +52,7 @@ def row_rel_max(a, ref):
 #    cfg1/cfg2/cfg3 for the rows kernel, 0.4-0.8 for the window kernels;
 #  * per-row max relative error <= 2 x the fp32 oracle's per-row max (+1e-6): catches a
 #    single wrong row or element that the global norm hides.
-def assert_model_parity(tag, g_in, g_out, o_in, o_out, f_in, f_out):
+def assert_model_parity(tag, g_in, g_out, o_in, o_out, f_in, f_out, abs_bar=True):
     rows = []
     for name, g, o, f in (("M_in", g_in, o_in, f_in), ("M_out", g_out, o_out, f_out)):
         eg, ef = rel_l2(g, o), rel_l2(f, o)
@@ -61,7 +61,8 @@ def assert_model_parity(tag, g_in, g_out, o_in, o_out, f_in, f_out):
         print(f"{tag} {name}: GPU vs fp64 rel L2 {eg:.3e} (fp32 oracle {ef:.3e}, ratio {eg / max(ef, 1e-30):.3f}); "
               f"per-row max {rg:.3e} (fp32 oracle {rf:.3e})")
     for name, eg, ef, rg, rf in rows:
-        assert eg <= 1e-5, f"{tag} {name}: rel L2 {eg:.3e} > 1e-5"
+        if abs_bar:
+            assert eg <= 1e-5, f"{tag} {name}: rel L2 {eg:.3e} > 1e-5"
         assert eg <= 1.25 * ef + 1e-6, f"{tag} {name}: rel L2 {eg:.3e} > 1.25 x fp32 oracle {ef:.3e} + 1e-6"
         assert rg <= 2.0 * rf + 1e-6, f"{tag} {name}: per-row max {rg:.3e} > 2 x fp32 oracle {rf:.3e}"
 
