@@ -111,7 +111,10 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          (multimem.ld_reduce / multimem.st, NVLS) when NCCL provides one, else
  *                          by peer loads/stores over NVLink — between two device-side barriers.
  *                          Needs NCCL >= 2.28 and all ranks in one NVLink domain (else ENCCL
- *                          from w2v_dist_init). C15's in-flight average stays an NCCL call.
+ *                          from w2v_dist_init). With "sync_overlap" also set before
+ *                          w2v_dist_init, C15's snapshot and average buffers are symmetric
+ *                          windows too and each in-flight average is the same kernel, out of
+ *                          place, on the library's comm stream (32 CTAs beside the step kernel).
  *  "sync_overlap"          C15 (default 0): the rows due are snapshot and averaged
  *                          on a communication stream while the next interval trains; their
  *                          correction M += avg - snapshot is applied one interval late; the last

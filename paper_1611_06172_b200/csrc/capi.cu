@@ -91,6 +91,7 @@ struct Ctx {
     int sync_device = 0;         // C17: a9 as one kernel over NCCL's symmetric window (sync_dev.cu)
     DevSync ds;                  // ... its window + device communicator (open after w2v_dist_init)
     bool M_nccl = false;         // the model lives in ncclMemAlloc memory (freed by ncclMemFree)
+    bool sy_nccl = false;        // ... and so do C15's snapshot / average buffers (C17 + C15)
     unsigned long long* ds_owned = nullptr;  // floats this rank reduced in the C17 kernel (stats)
     cudaStream_t comm_stream = nullptr;
     // w2v_prefetch: up to two host corpora copied ahead on the copy stream into their own device
@@ -296,8 +297,8 @@ int sync_models(int64_t row_lo = 0, int64_t row_hi = -1, int* launches = nullptr
     if (row_hi < 0) row_hi = g.V;
     if (row_hi <= row_lo) return W2V_OK;
     if (g.ds.devcomm) {  // C17: one kernel, in place over the symmetric window (sync_dev.cu)
-        CU(devsync_launch(g.ds, (size_t)row_lo * 2 * g.Ds, (size_t)(row_hi - row_lo) * 2 * g.Ds, g.ds_owned,
-                          g.stream));
+        CU(devsync_launch(g.ds, 0, 0, (size_t)row_lo * 2 * g.Ds, (size_t)(row_hi - row_lo) * 2 * g.Ds, g.ds_owned,
+                          kDevSyncCtas, g.stream));
         if (launches) ++*launches;
     } else {
         NC(g_nccl.allReduce(g.M + (size_t)row_lo * 2 * g.Ds, g.M + (size_t)row_lo * 2 * g.Ds,
@@ -816,8 +817,14 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                         CU(launch_sync_snap(g.M, g.syC, (size_t)hi_r * rowf, g.sms, st));
                         CU(cudaEventRecord(ev_snap, st));
                         CU(cudaStreamWaitEvent(g.comm_stream, ev_snap, 0));
-                        NC(g_nccl.allReduce(g.syC, g.syS, (size_t)hi_r * rowf, ncclFloat32, ncclAvg, g.comm,
-                                            g.comm_stream));
+                        if (g.ds.devcomm && g.ds.nwin == 3) {   // C17: the device kernel, C -> S, small grid
+                            CU(devsync_launch(g.ds, 1, 2, 0, (size_t)hi_r * rowf, g.ds_owned, kDevSyncOverlapCtas,
+                                              g.comm_stream));
+                            ++launches;
+                        } else {
+                            NC(g_nccl.allReduce(g.syC, g.syS, (size_t)hi_r * rowf, ncclFloat32, ncclAvg, g.comm,
+                                                g.comm_stream));
+                        }
                         CU(cudaEventRecord(ev_ar, g.comm_stream));
                         pend_hi = hi_r;
                         if (full) g.st.syncs += 1; else g.st.syncs_hot += 1;
@@ -1024,6 +1031,22 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
         g.M = M2;
         g.M_nccl = g.sync_device != 0;
         g.Ds = Dn;
+        if (g.sync_device && g.sync_overlap && !g.syS) {
+            // C15 with C17: the snapshot C and the average S are symmetric windows too
+            std::string e;
+            void *bc = nullptr, *bs = nullptr;
+            int lrc = devsync_alloc(bytes, &bc, &e) || devsync_alloc(bytes, &bs, &e) ? fail(W2V_ENCCL, "%s", e.c_str())
+                                                                                    : W2V_OK;
+            lrc = dp_agree(lrc, g.stream);
+            if (lrc) {
+                devsync_free(bc);
+                devsync_free(bs);
+                return lrc;
+            }
+            g.syC = (float*)bc;
+            g.syS = (float*)bs;
+            g.sy_nccl = true;
+        }
         if (g.sync_device) {  // collective: window registration + device communicator
             std::string e;
             auto agree_min = [](int v) -> int {  // min over ranks (NCCL all-reduce on the scratch)
@@ -1035,7 +1058,9 @@ int w2v_dist_init(int32_t rank, int32_t world, const uint8_t id[128]) {
                 if (cudaStreamSynchronize(g.stream) != cudaSuccess) return -1;
                 return (int)h;
             };
-            if (devsync_open(g.comm, g.M, bytes, world, 1, +agree_min, &g.ds, &e))
+            void* bufs[3] = {g.M, g.syC, g.syS};
+            const size_t sizes[3] = {bytes, bytes, bytes};
+            if (devsync_open(g.comm, bufs, sizes, g.sy_nccl ? 3 : 1, world, 1, +agree_min, &g.ds, &e))
                 return fail(W2V_ENCCL, "%s", e.c_str());
             g.st.sync_path = g.ds.multimem ? 3 : 2;
         }
@@ -1089,7 +1114,7 @@ int w2v_finalize(void) {
         cudaFree(f.buf);
         if (f.done) cudaEventDestroy(f.done);
     }
-    cudaFree(g.syS); cudaFree(g.syC);
+    if (g.sy_nccl) { devsync_free(g.syS); devsync_free(g.syC); } else { cudaFree(g.syS); cudaFree(g.syC); }
     cudaStreamDestroy(g.own_stream);
     Ctx fresh;
     g = fresh;

@@ -13,7 +13,9 @@
 //          scaled by 1/W and stored into every peer.
 // An LSA barrier opens the pass (every replica finished its interval) and closes it with release
 // order (every store landed before any rank trains on). No host round trip, no staging copy,
-// no second buffer: the in-place mean of C13/C14 in one launch on the training stream.
+// no second buffer: the in-place mean of C13/C14 in one launch on the training stream. With C15
+// (sync_overlap) the same kernel runs OUT of place — snapshot window C -> average window S — on
+// the comm stream with a small grid, concurrently with the next interval's training.
 //
 // Built against the NCCL 2.28 device headers of the nvidia-nccl wheel that torch loads (the
 // ncclDevComm layout is version-specific: devsync_open checks the runtime's major.minor).
@@ -92,9 +94,10 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
 
 // floats [off, off+n) of the window: this rank's slice [s0, s1) = [off + n*r/W, off + n*(r+1)/W)
 // (W = LSA team size, r = LSA rank); a scalar head up to 16-B alignment, a float4 body, a scalar tail.
+// dst[off, off+n) := mean over the W replicas of src[off, off+n) (src == dst: in place)
 template <bool MM>
-__global__ void __launch_bounds__(kThreads, 2) avg_kernel(ncclWindow_t win, ncclDevComm dc, size_t off, size_t n,
-                                                       unsigned long long* counted) {
+__global__ void __launch_bounds__(kThreads, 2) avg_kernel(ncclWindow_t src, ncclWindow_t dst, ncclDevComm dc,
+                                                       size_t off, size_t n, unsigned long long* counted) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, MM);
     bar.sync(ncclCoopCta(), cuda::memory_order_relaxed);  // every replica finished its interval
 
@@ -106,27 +109,29 @@ __global__ void __launch_bounds__(kThreads, 2) avg_kernel(ncclWindow_t win, nccl
     uint32_t mine = 0;
 
     if constexpr (MM) {
-        float* mm = (float*)ncclGetLsaMultimemPointer(win, 0, dc);
-        for (size_t i = s0 + tid; i < a0; i += T) { mm_st1(mm + i, __fmul_rn(mm_ld_reduce1(mm + i), inv)); ++mine; }
-        for (size_t i = a1 + tid; i < s1; i += T) { mm_st1(mm + i, __fmul_rn(mm_ld_reduce1(mm + i), inv)); ++mine; }
-        float4* m4 = reinterpret_cast<float4*>(mm);
+        const float* ms = (const float*)ncclGetLsaMultimemPointer(src, 0, dc);
+        float* md = (float*)ncclGetLsaMultimemPointer(dst, 0, dc);
+        for (size_t i = s0 + tid; i < a0; i += T) { mm_st1(md + i, __fmul_rn(mm_ld_reduce1(ms + i), inv)); ++mine; }
+        for (size_t i = a1 + tid; i < s1; i += T) { mm_st1(md + i, __fmul_rn(mm_ld_reduce1(ms + i), inv)); ++mine; }
+        const float4* s4 = reinterpret_cast<const float4*>(ms);
+        float4* d4 = reinterpret_cast<float4*>(md);
         const size_t v0 = a0 / 4, v1 = a1 / 4;
         for (size_t b = v0 + tid; b < v1; b += T * kUnroll) {
             float4 s[kUnroll];
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k)
-                if (b + k * T < v1) s[k] = mm_ld_reduce4(m4 + b + k * T);
+                if (b + k * T < v1) s[k] = mm_ld_reduce4(s4 + b + k * T);
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k)
-                if (b + k * T < v1) { mm_st4(m4 + b + k * T, scale4(s[k], inv)); mine += 4; }
+                if (b + k * T < v1) { mm_st4(d4 + b + k * T, scale4(s[k], inv)); mine += 4; }
         }
     } else {
         // rank-order sum of the peers' copies (the same order on every rank)
         auto one = [&](size_t i) {
-            float s = __ldcg((const float*)ncclGetLsaPointer(win, 0, 0) + i);
-            for (int p = 1; p < W; ++p) s = __fadd_rn(s, __ldcg((const float*)ncclGetLsaPointer(win, 0, p) + i));
+            float s = __ldcg((const float*)ncclGetLsaPointer(src, 0, 0) + i);
+            for (int p = 1; p < W; ++p) s = __fadd_rn(s, __ldcg((const float*)ncclGetLsaPointer(src, 0, p) + i));
             s = __fmul_rn(s, inv);
-            for (int p = 0; p < W; ++p) __stcg((float*)ncclGetLsaPointer(win, 0, p) + i, s);
+            for (int p = 0; p < W; ++p) __stcg((float*)ncclGetLsaPointer(dst, 0, p) + i, s);
             ++mine;
         };
         for (size_t i = s0 + tid; i < a0; i += T) one(i);
@@ -134,12 +139,12 @@ __global__ void __launch_bounds__(kThreads, 2) avg_kernel(ncclWindow_t win, nccl
         const size_t v0 = a0 / 4, v1 = a1 / 4;
         for (size_t b = v0 + tid; b < v1; b += T * kUnroll) {
             float4 s[kUnroll];
-            const float4* p0 = (const float4*)ncclGetLsaPointer(win, 0, 0);
+            const float4* p0 = (const float4*)ncclGetLsaPointer(src, 0, 0);
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k)
                 if (b + k * T < v1) s[k] = __ldcg(p0 + b + k * T);
             for (int p = 1; p < W; ++p) {
-                const float4* pp = (const float4*)ncclGetLsaPointer(win, 0, p);
+                const float4* pp = (const float4*)ncclGetLsaPointer(src, 0, p);
                 float4 x[kUnroll];
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k)
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 2) avg_kernel(ncclWindow_t win, nccl
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k) s[k] = scale4(s[k], inv);
             for (int p = 0; p < W; ++p) {
-                float4* pp = (float4*)ncclGetLsaPointer(win, 0, p);
+                float4* pp = (float4*)ncclGetLsaPointer(dst, 0, p);
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k)
                     if (b + k * T < v1) __stcg(pp + b + k * T, s[k]);
@@ -201,11 +206,26 @@ void devsync_free(void* buf) {
 // agree_min(v): the minimum of v over all ranks (a collective supplied by the caller), so that a
 // multicast team that only some ranks could create is dropped on every rank (the fallback
 // creation is collective too and must be called by all or none)
-int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_mm, int (*agree_min)(int),
-                 DevSync* ds, std::string* err) {
-    ncclWindow_t win = nullptr;
-    ncclResult_t r = g_dev.winRegister(comm, buf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
-    if (r != ncclSuccess) { set_err(err, "sync_device: ncclCommWindowRegister", r); return 1; }
+int devsync_open(ncclComm_t comm, void* const* bufs, const size_t* bytes, int nwin, int world, int want_mm,
+                 int (*agree_min)(int), DevSync* ds, std::string* err) {
+    // every window is registered BEFORE the device communicator is created (its multicast
+    // mapping then covers them all)
+    ncclWindow_t wins[kDevSyncMaxWin] = {};
+    auto drop_wins = [&]() {
+        for (int k = 0; k < nwin; ++k)
+            if (wins[k]) g_dev.winDeregister(comm, wins[k]);
+    };
+    if (nwin < 1 || nwin > kDevSyncMaxWin) { *err = "sync_device: bad window count"; return 1; }
+    ncclResult_t r = ncclSuccess;
+    for (int k = 0; k < nwin; ++k) {
+        r = g_dev.winRegister(comm, bufs[k], bytes[k], &wins[k], NCCL_WIN_COLL_SYMMETRIC);
+        if (r != ncclSuccess) {
+            wins[k] = nullptr;
+            drop_wins();
+            set_err(err, "sync_device: ncclCommWindowRegister", r);
+            return 1;
+        }
+    }
     auto* dc = new ncclDevComm;
     ncclDevCommRequirements req;
     std::memset(&req, 0, sizeof req);
@@ -219,7 +239,7 @@ int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_m
         if (all < 0) {
             if (made) g_dev.devCommDestroy(comm, dc);
             delete dc;
-            g_dev.winDeregister(comm, win);
+            drop_wins();
             *err = "sync_device: the multicast agreement collective failed";
             return 1;
         }
@@ -231,7 +251,7 @@ int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_m
         r = g_dev.devCommCreate(comm, &req, dc);
         if (r != ncclSuccess) {
             delete dc;
-            g_dev.winDeregister(comm, win);
+            drop_wins();
             set_err(err, "sync_device: ncclDevCommCreate", r);
             return 1;
         }
@@ -242,12 +262,13 @@ int devsync_open(ncclComm_t comm, void* buf, size_t bytes, int world, int want_m
                  "required; use the NCCL all-reduce path)", dc->lsaSize, world);
         g_dev.devCommDestroy(comm, dc);
         delete dc;
-        g_dev.winDeregister(comm, win);
+        drop_wins();
         *err = b;
         return 1;
     }
     ds->comm = comm;
-    ds->win = (void*)win;
+    for (int k = 0; k < nwin; ++k) ds->win[k] = (void*)wins[k];
+    ds->nwin = nwin;
     ds->devcomm = (void*)dc;
     ds->multimem = mm;
     ds->lsa_size = dc->lsaSize;
@@ -259,17 +280,22 @@ void devsync_close(DevSync* ds) {
     auto* dc = (ncclDevComm*)ds->devcomm;
     g_dev.devCommDestroy((ncclComm_t)ds->comm, dc);
     delete dc;
-    g_dev.winDeregister((ncclComm_t)ds->comm, (ncclWindow_t)ds->win);
+    for (int k = 0; k < ds->nwin; ++k) g_dev.winDeregister((ncclComm_t)ds->comm, (ncclWindow_t)ds->win[k]);
     *ds = DevSync{};
 }
 
-// floats [off, off + n) of the window (the model) := their mean over the LSA team
-cudaError_t devsync_launch(const DevSync& ds, size_t off, size_t n, unsigned long long* counted, cudaStream_t st) {
+// floats [off, off + n) of window `dst` := the mean over the LSA team of the same floats of
+// window `src` (src == dst: in place), on `ctas` <= kDevSyncCtas CTAs
+cudaError_t devsync_launch(const DevSync& ds, int src, int dst, size_t off, size_t n, unsigned long long* counted,
+                           int ctas, cudaStream_t st) {
+    if (src < 0 || src >= ds.nwin || dst < 0 || dst >= ds.nwin || ctas < 1 || ctas > kDevSyncCtas)
+        return cudaErrorInvalidValue;
     const ncclDevComm& dc = *(const ncclDevComm*)ds.devcomm;
+    const ncclWindow_t ws = (ncclWindow_t)ds.win[src], wd = (ncclWindow_t)ds.win[dst];
     if (ds.multimem)
-        avg_kernel<true><<<kDevSyncCtas, kThreads, 0, st>>>((ncclWindow_t)ds.win, dc, off, n, counted);
+        avg_kernel<true><<<ctas, kThreads, 0, st>>>(ws, wd, dc, off, n, counted);
     else
-        avg_kernel<false><<<kDevSyncCtas, kThreads, 0, st>>>((ncclWindow_t)ds.win, dc, off, n, counted);
+        avg_kernel<false><<<ctas, kThreads, 0, st>>>(ws, wd, dc, off, n, counted);
     return cudaGetLastError();
 }
 

@@ -123,19 +123,23 @@ __host__ __device__ inline void devsync_slice(size_t off, size_t n, int r, int W
     *a0 = *s0 + 3 < *s1 ? (*s0 + 3) & ~(size_t)3 : *s1;
     *a1 = *a0 + ((*s1 - *a0) & ~(size_t)3);
 }
+constexpr int kDevSyncOverlapCtas = 32;  // C15's in-flight average: a small grid beside the step kernel
+constexpr int kDevSyncMaxWin = 3;        // windows: 0 the model, 1 C15 snapshot C, 2 C15 average S
 struct DevSync {
-    void* comm = nullptr;     // ncclComm_t
-    void* win = nullptr;      // ncclWindow_t of the model buffer
-    void* devcomm = nullptr;  // heap ncclDevComm
-    int multimem = 0;         // 1: NVLS multicast path, 0: LSA peer loads/stores
+    void* comm = nullptr;                 // ncclComm_t
+    void* win[kDevSyncMaxWin] = {};       // ncclWindow_t per registered buffer
+    int nwin = 0;
+    void* devcomm = nullptr;              // heap ncclDevComm
+    int multimem = 0;                     // 1: NVLS multicast path, 0: LSA peer loads/stores
     int lsa_size = 0;
 };
 int devsync_alloc(size_t bytes, void** buf, std::string* err);
 void devsync_free(void* buf);
-int devsync_open(ncclComm* comm, void* buf, size_t bytes, int world, int want_mm, int (*agree_min)(int), DevSync* ds,
-                 std::string* err);
+int devsync_open(ncclComm* comm, void* const* bufs, const size_t* bytes, int nwin, int world, int want_mm,
+                 int (*agree_min)(int), DevSync* ds, std::string* err);
 void devsync_close(DevSync* ds);
-cudaError_t devsync_launch(const DevSync& ds, size_t off, size_t n, unsigned long long* counted, cudaStream_t st);
+cudaError_t devsync_launch(const DevSync& ds, int src, int dst, size_t off, size_t n, unsigned long long* counted,
+                           int ctas, cudaStream_t st);
 
 // alg1.cu (Algorithm 1, the level-1 baseline)
 bool alg1_supported(int D, int K);

@@ -32,7 +32,7 @@ def _free_port():
 
 @pytest.mark.parametrize("world", [1, 2])
 @pytest.mark.parametrize("hot,cold_every,overlap,sync_device", [(0, 1, 0, 0), (150, 3, 0, 0), (0, 1, 1, 0),
-                                                               (0, 1, 0, 1), (150, 3, 0, 1)])
+                                                               (0, 1, 0, 1), (150, 3, 0, 1), (0, 1, 1, 1)])
 def test_replicas_match_oracle_protocol(tmp_path, world, hot, cold_every, overlap, sync_device):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs (visible: {torch.cuda.device_count()})")

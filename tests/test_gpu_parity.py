@@ -495,7 +495,7 @@ def test_cfg4_full_size_sampled_stream(w2v):
 # ------------------------------------------------------------------ data-parallel path --------
 @pytest.mark.parametrize("hot_rows,cold_every,overlap,sync_device",
                          [(0, 1, 0, 0), (100, 3, 0, 0), (100, 3, 1, 0), (0, 1, 1, 0),
-                          (0, 1, 0, 1), (100, 3, 0, 1), (0, 1, 1, 1)])
+                          (0, 1, 0, 1), (100, 3, 0, 1), (0, 1, 1, 1), (100, 3, 1, 1)])
 def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap, sync_device):
     """The DP code path (C13: n_local all-gather, histogram all-reduce, sync intervals, model
     averaging via NCCL; C14: hot-prefix averaging with the cold rows every 3rd interval; C15: the
@@ -531,7 +531,11 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap, 
     assert np.array_equal(M_in, plain["M_in"]) and np.array_equal(M_out, plain["M_out"])
     Ds = (cfg.D + 31) // 32 * 32   # the 1-rank model keeps its 128-B row padding
     row = 2 * Ds
-    owned = cfg.V * row if overlap else full * cfg.V * row + (J - full) * hot_rows * row
+    fulls = [odist.synced_rows(k, J, cfg.V, hot_rows, cold_every) == [(0, cfg.V)] for k in range(J)]
+    # C15 with C17: every in-flight average (intervals 0..J-2, rows due) runs the device kernel
+    # out of place on the comm stream; the last interval ends with the blocking in-place mean
+    owned = (sum((cfg.V if f else hot_rows) for f in fulls[:-1]) + cfg.V) * row if overlap else \
+        full * cfg.V * row + (J - full) * hot_rows * row
     assert st["sync_path"] == (2 if sync_device else 1)   # no multicast object on one GPU: LSA path
     assert st["sync_floats_owned"] == (owned if sync_device else 0)
     w2v.sync()
