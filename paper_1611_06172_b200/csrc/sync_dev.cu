@@ -18,7 +18,7 @@
 // the comm stream with a small grid, concurrently with the next interval's training.
 //
 // Built against the NCCL 2.28 device headers of the nvidia-nccl wheel that torch loads (the
-// ncclDevComm layout is version-specific: devsync_open checks the runtime's major.minor).
+// ncclDevComm layout is version-specific: devsync_alloc checks the runtime's major.minor).
 #include <nccl.h>
 #include <nccl_device.h>
 #include <dlfcn.h>
