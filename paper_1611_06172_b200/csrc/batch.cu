@@ -129,19 +129,31 @@ __global__ void __launch_bounds__(32 * kBatchWarps) batch_kernel(const StepParam
             continue;
         }
 
-        // ---- a2: K negatives per kept target (C7). Lane u handles draw d = u % K of target
-        // m = u / K, assuming no rejection before it; a target whose first K draws contain a
-        // rejection (x == target) is redone by one lane with the literal sequential rule.
+        // ---- a2: K negatives per kept target (C7). Lane u handles Philox block j = u % KB of
+        // target m = u / KB (KB = ceil(K/2)): its two u64 halves are draws 2j and 2j+1 (C1), so
+        // each block is computed once and each lane runs two independent inverse-CDF chains —
+        // assuming no rejection before them; a target whose first K draws contain a rejection
+        // (x == target) is redone by one lane with the literal sequential rule.
         for (int i = lane; i < (nk + 31) / 32; i += 32) fix[i] = 0u;
         __syncwarp();
         int32_t* neg = p.bt_neg + rel * Lp * KS;
-        for (int u = lane; u < nk * K; u += 32) {
-            const int m = u / K, d = u - m * K;
+        const int KB = (K + 1) >> 1;
+        for (int u = lane; u < nk * KB; u += 32) {
+            const int m = u / KB, j = u - m * KB;
             const int64_t pp = c0 + (kinfo[m] >> 8);
             const int32_t tw = kid[m];
-            const int32_t x = neg_draw(p, e, pp, (uint32_t)d, PV, gshift);
-            if (x != tw || p.allow_tn) neg[m * KS + d] = x;
-            else atomicOr(fix + (m >> 5), 1u << (m & 31));
+            const U4 r = philox(p.seed, kTagNeg, e, (uint64_t)pp, (uint32_t)j);
+            const int32_t x0 = invcdf_guided(p.P, p.G, gshift, __umul64hi(((uint64_t)r.y << 32) | r.x, PV));
+            const bool two = 2 * j + 1 < K;
+            const int32_t x1 = two ? invcdf_guided(p.P, p.G, gshift, __umul64hi(((uint64_t)r.w << 32) | r.z, PV)) : 0;
+            bool bad = false;
+            if (x0 != tw || p.allow_tn) neg[m * KS + 2 * j] = x0;
+            else bad = true;
+            if (two) {
+                if (x1 != tw || p.allow_tn) neg[m * KS + 2 * j + 1] = x1;
+                else bad = true;
+            }
+            if (bad) atomicOr(fix + (m >> 5), 1u << (m & 31));
         }
         __syncwarp();
         for (int m = lane; m < nk; m += 32) {
