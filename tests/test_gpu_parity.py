@@ -543,6 +543,12 @@ def test_nccl_one_rank_dp_path_equals_plain(w2v, hot_rows, cold_every, overlap, 
     assert np.array_equal(M_in, plain["M_in"])
     if sync_device:
         assert w2v.get_stats()["sync_floats_owned"] == owned + cfg.V * row
+        # the model now lives in ncclMemAlloc (VMM) memory: embeddings I/O round-trips exactly
+        z = np.ascontiguousarray(M_out[::-1])
+        w2v.set_embeddings(0, z)
+        back = np.empty_like(z)
+        w2v.get_embeddings(0, back)
+        assert np.array_equal(back, z)
 
 
 def test_rowpath_only_measurement_mode(w2v):
