@@ -115,6 +115,10 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          w2v_dist_init, C15's snapshot and average buffers are symmetric
  *                          windows too and each in-flight average is the same kernel, out of
  *                          place, on the library's comm stream (32 CTAs beside the step kernel).
+ *  "tma_gather"            1 (default): the rows kernel gathers 4 rows per TMA tile::gather4
+ *                          instruction where its slab allows (D <= 256 packed, 2*window and the
+ *                          output tile multiples of 4: cfg4's D = 128, K = 15, window 8); 0 =
+ *                          one cp.async.bulk per row everywhere. Same data either way.
  *  "sync_overlap"          C15 (default 0): the rows due are snapshot and averaged
  *                          on a communication stream while the next interval trains; their
  *                          correction M += avg - snapshot is applied one interval late; the last

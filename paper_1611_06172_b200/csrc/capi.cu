@@ -152,6 +152,7 @@ struct Ctx {
     uint32_t* bt_redo = nullptr;
     cudaStream_t side = nullptr;
     int check_finite = 1;   // NaN/Inf scan of the model after every w2v_train (W2V_ENUMERIC)
+    int tma_gather = 1;     // rows kernel: TMA tile::gather4 where step_tma_gather_ok (option)
     int overlap_batch = 0;  // option "overlap_batch" (measured slower on B200: DESIGN.md §8)
     // debug
     uint8_t *dbg_keep = nullptr, *dbg_b = nullptr, *dbg_N = nullptr;
@@ -416,6 +417,7 @@ int w2v_set_option(const char* key, int64_t v) {
     else if (k == "rowpath_only") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "rowpath_only must be 0/1"); g.rowpath_only = (int)v; }
     else if (k == "scatter_wait") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "scatter_wait must be 0/1"); g.scatter_wait = (int)v; }
     else if (k == "ring_writeback") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "ring_writeback must be 0/1"); g.ring_writeback = (int)v; }
+    else if (k == "tma_gather") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "tma_gather must be 0/1"); g.tma_gather = (int)v; }
     else if (k == "check_finite") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "check_finite must be 0/1"); g.check_finite = (int)v; }
     else if (k == "overlap_batch") { if (v != 0 && v != 1) return fail(W2V_EINVAL, "overlap_batch must be 0/1"); g.overlap_batch = (int)v; }
     else if (k == "kernel") { if (v < 0 || v > 4) return fail(W2V_EINVAL, "kernel must be 0 (auto), 1 (rows), 2 (window), 3 (window, warp-specialised) or 4 (ring, TMEM originals)"); g.kernel = (int)v; }
@@ -622,6 +624,31 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
     p.rowpath_only = g.rowpath_only;
     p.ring_delta = g.ring_writeback;
     p.scatter_wait = g.scatter_wait;
+    // rows kernel gathers through TMA tile::gather4 (4 rows per instruction) where the slab
+    // layout allows it: the model as a 2-D fp32 tensor [V][2*Ds], box D x 1
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof tmap);
+    p.tma_gather = 0;
+    if (g.tma_gather && g.algorithm == 0 && step_tma_gather_ok(g.D, g.K, g.window)) {
+        typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        static Encode encode = nullptr;
+        if (!encode) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess)
+                encode = (Encode)fn;
+            cudaGetLastError();
+        }
+        const cuuint64_t dims[2] = {(cuuint64_t)2 * g.Ds, (cuuint64_t)g.V};
+        const cuuint64_t strides[1] = {(cuuint64_t)2 * g.Ds * sizeof(float)};
+        const cuuint32_t box[2] = {(cuuint32_t)g.D, 1}, es[2] = {1, 1};
+        if (encode && encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.M, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            p.tma_gather = 1;
+    }
     {   // cache-aware roofline statistics: the hot prefix whose half-rows of both matrices fill L2
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g.device);
@@ -786,7 +813,7 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
                 CU(mark(0));
                 CU(kern == 0 ? launch_alg1(p, ctas, st) : kern == 4 ? launch_ring(p, ctas, ring_units, st)
                    : kern == 3 ? launch_wg(p, ctas, st)
-                   : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st));  // a3-a8
+                      : use_win ? launch_win(p, ctas, st) : launch_step(p, ctas, st, p.tma_gather ? &tmap : nullptr));  // a3-a8
                 CU(mark(0));
                 if (ovl) CU(cudaEventRecord(ev_sdone[set], st));
                 launches += 2;

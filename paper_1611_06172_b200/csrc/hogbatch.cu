@@ -23,6 +23,7 @@
 // "write back at the end of the GEMM" is the scatter of a7.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "hogbatch_common.cuh"
 
@@ -85,9 +86,12 @@ __host__ __device__ constexpr int kring_slots(int window) {
 // The packed instance for the paper's D=300 (RSC=300) saves 20 floats per row — what lets an 11th
 // work unit fit per SM — at the cost of a predicate on each lane's last float2 column.
 // TK: the mode-2 (NEXT-4) ticketed instance; the others carry none of its code or registers
+// tmap (p.tma_gather): the model as a 2-D fp32 tensor [V][2*Ds] with a box of D x 1; a group of 4
+// rows of one matrix lands as 4 consecutive slab rows (RS == D) with one tile::gather4
 template <int CP2, int KP1MAX, int RSC, bool TK>
-__global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepParams p,
+                                                                     const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem[];
     constexpr int TI = 32 / KP1MAX;  // inputs per reduce-scatter tile
     const int lane = threadIdx.x & 31;
     unsigned char* wbase = smem + (threadIdx.x >> 5) * p.warp_bytes;
@@ -281,6 +285,29 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
             }
             // ---------------- a3: gather the snapshot rows (one bulk copy per row)
             W2V_T(long long t1 = clock64();)
+            if (p.tma_gather) {
+                // groups of 4 rows per TMA instruction (SURVEY.md §8(a) "Gather engines"); a
+                // group's missing rows repeat its last row (landing in slab rows the compute
+                // and the scatter never use: the slab holds 2w >= 4*ceil(N/4) A rows and
+                // KP1MAX >= 4*ceil((K+1)/4) B rows, step_tma_gather_ok)
+                const int ga = (N + 3) >> 2, gb = (KP1 + 3) >> 2;
+                if (lane == 0) mbar_arrive_expect_tx(mbar, (uint32_t)(4 * (ga + gb)) * rowbytes);
+                __syncwarp();
+                if (lane < ga + gb) {
+                    const bool isA = lane < ga;
+                    const int r0 = isA ? 4 * lane : N + 4 * (lane - ga), rend = isA ? N : R;
+                    int32_t id[4];
+                    bool hot = false;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        id[k] = rowid[r0 + k < rend ? r0 + k : rend - 1];
+                        hot |= id[k] < (isA ? p.hot_rows_in : p.hot_rows);
+                    }
+                    tma_gather4_hint(isA ? As + 4 * lane * RS : Bs + 4 * (lane - ga) * RS, &tmap, isA ? 0 : Ds,
+                                     id, mbar, hot ? pol_hot : pol_cold);
+                }
+                for (int r = lane; r < R; r += 32) st_cold += rowid[r] >= p.cold_from;
+            } else {
 #ifndef W2V_ABL_NOGATHER
             if (lane == 0) mbar_arrive_expect_tx(mbar, (uint32_t)R * rowbytes);
 #else
@@ -297,6 +324,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
 #else
                 (void)dst; (void)id;
 #endif
+            }
             }
             // while the rows fly: fetch negatives ahead, build the next target's row list, alpha.
             // One cp.async group per target (possibly empty); targets fetched at iteration m' are
@@ -539,7 +567,7 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
     }
 }
 
-using KernelFn = void (*)(const StepParams);
+using KernelFn = void (*)(const StepParams, const CUtensorMap);
 
 struct Inst {
     int cp2, kp1, rs;  // rs: packed row stride (the instance serves D == rs only), 0 = padded
@@ -607,7 +635,10 @@ size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, in
     // long chunks: a kring_slots(window)-slot ring (window <= 32), else read from the batch stream
     const int Lps = Lp <= kSmemChunk ? Lp : window <= 32 ? kring_slots(window) : 0;
     const size_t ids = 16 + (size_t)(2 * Lps + 2 * R + kNegRows * (K > 0 ? K : 1)) * 4 + gfl * 4;
-    const size_t off = (ids + 15) / 16 * 16;  // 16-B aligned slab (bulk copies); every byte counts
+    // 16-B aligned slab (bulk copies; every byte counts), 128-B aligned where the TMA gather4
+    // path may run (tensor destinations)
+    const size_t align = step_tma_gather_ok(D, K, window) ? 128 : 16;
+    const size_t off = (ids + align - 1) / align * align;
     if (slab_offset) *slab_offset = (int32_t)off;
     const size_t end = off + (size_t)(in->kp1 + 2 * window) * RS * 4;
     if (tick_offset) {  // mode 2: + a ticket table [Lp][2w+K+1] u32 after the slab
@@ -627,14 +658,27 @@ int step_max_ctas_per_sm(const StepParams& p) {
     return n;
 }
 
-cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st) {
+cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st, const CUtensorMap* tmap) {
     const Inst* in = pick(p.D, p.K);
     if (!in) return cudaErrorInvalidValue;
+    if (p.tma_gather && !tmap) return cudaErrorInvalidValue;
     const KernelFn fn = p.deterministic == 2 ? in->fn_tk : in->fn;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.warp_bytes);
     if (e != cudaSuccess) return e;
-    fn<<<ctas, 32, p.warp_bytes, st>>>(p);
+    CUtensorMap none;
+    std::memset(&none, 0, sizeof none);
+    fn<<<ctas, 32, p.warp_bytes, st>>>(p, tmap ? *tmap : none);
     return cudaGetLastError();
+}
+
+// TMA tile::gather4 for the rows kernel: one box of D fp32 columns per row (D <= 256, 16-B
+// multiple), slab rows packed at RS == D, and whole groups of 4 fitting the slab: 2*window and
+// KP1MAX multiples of 4
+bool step_tma_gather_ok(int D, int K, int window) {
+    const Inst* in = pick(D, K);
+    if (!in) return false;
+    const int RS = in->rs > 0 ? in->rs : 64 * in->cp2;
+    return D <= 256 && RS == D && (2 * window) % 4 == 0 && in->kp1 % 4 == 0;
 }
 
 }  // namespace w2v

@@ -2,6 +2,7 @@
 // written from the contract text, not from the oracle's source.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace w2v {
@@ -102,6 +103,16 @@ __device__ __forceinline__ void bulk_g2s_hint(void* sdst, const void* gsrc, uint
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(sdst)),
         "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+// TMA tile::gather4: rows r[0..3], columns [col, col + box) of the 2-D tensor `tmap` into 4
+// consecutive box rows at sdst (128-B aligned), completing on the mbarrier
+__device__ __forceinline__ void tma_gather4_hint(void* sdst, const CUtensorMap* tmap, int col, const int32_t (&r)[4],
+                                                 uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(sdst)),
+        "l"(tmap), "r"(col), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {

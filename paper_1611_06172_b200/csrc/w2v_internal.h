@@ -1,6 +1,7 @@
 // w2v_internal.h — structures shared by the library's translation units (not part of the ABI).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <string>
 
@@ -79,6 +80,7 @@ struct StepParams {
     int64_t cold_from;    // statistics: row touches with id >= cold_from are counted as "cold" (the
                           // ids beyond an L2-sized hot prefix; the cache-aware roofline's B_cold)
     int32_t algorithm;    // 0 HogBatch (shared negatives), 1 Alg.1 (per-input negatives, alg1.cu)
+    int32_t tma_gather;   // rows kernel: gather 4 rows per TMA tile::gather4 (step_tma_gather_ok)
     int32_t* dbg_a1neg;   // Alg.1 debug: [len][2*window][K] per-input negatives
 };
 
@@ -155,7 +157,8 @@ cudaError_t launch_ring(const StepParams& p, int ctas, int units, cudaStream_t s
 
 // hogbatch.cu (per-target rows; any window)
 bool step_supported(int D, int K);
-cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st);
+cudaError_t launch_step(const StepParams& p, int ctas, cudaStream_t st, const CUtensorMap* tmap);
+bool step_tma_gather_ok(int D, int K, int window);
 int step_max_ctas_per_sm(const StepParams& p);
 size_t step_warp_bytes(int L, int window, int K, int D, int32_t* slab_offset, int32_t* tick_offset = nullptr);
 void step_phase_report();  // (experiment builds with W2V_PHASE_TIMING) prints per-phase cycles

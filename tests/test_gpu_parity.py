@@ -768,3 +768,30 @@ def test_ring_delta_writeback_parity(w2v, case):
     for k in ("words", "targets", "row_touches", "loss_pairs"):
         assert g["stats"][k] == o_st[k], k
     assert_model_parity(f"{case}[:{n}] ring delta write-back", g["M_in"], g["M_out"], o_in, o_out, f_in, f_out)
+
+
+@pytest.mark.parametrize("V,D,window,K,L,n", [
+    (300, 128, 8, 15, 1000, 6_000),   # cfg4's tile: K+1 = KP1MAX = 16, N <= 16 (ragged last group)
+    (500, 64, 2, 3, 37, 4_000),       # KP1MAX 4, N <= 4
+    (400, 192, 6, 5, 100, 5_000),     # K+1 = 6 in a KP1MAX 8 tile: two padded B rows per target
+    (200, 256, 4, 1, 20, 3_000),      # widest box (256 floats), K+1 = 2 in a KP1MAX 4 tile
+])
+def test_tma_gather4_equals_bulk_rows(w2v, V, D, window, K, L, n):
+    """The rows kernel's TMA tile::gather4 path (4 rows per instruction; groups padded with their
+    last row into slab rows the compute never reads) gathers exactly what the per-row bulk copies
+    gather: deterministic mode is bit-identical with tma_gather 1 and 0, and matches the oracle."""
+    ids = inputs.Corpus("iid", V, 1.0, 77).tokens(0, n)
+    runs = {}
+    for tma in (1, 0):
+        w2v.finalize()
+        runs[tma] = run_gpu(w2v, ids, V, D, window, K, 0.025, 1e-3, 5, L, opts={"tma_gather": tma})
+    assert np.array_equal(runs[1]["M_in"], runs[0]["M_in"]) and np.array_equal(runs[1]["M_out"], runs[0]["M_out"])
+    o_in, o_out, o_st, _ = oracle.train(ids, V, D, window, K, 0.025, 1e-3, 5, L)
+    f_in, f_out, _, _ = oracle.train(ids, V, D, window, K, 0.025, 1e-3, 5, L, prec="f32")
+    assert runs[1]["stats"]["row_touches"] == o_st["row_touches"]
+    assert_model_parity(f"tma V={V} D={D} w={window} K={K}", runs[1]["M_in"], runs[1]["M_out"], o_in, o_out, f_in,
+                        f_out)
+    # Hogwild (all SMs) through the TMA path: the same batch stream, a finite model
+    w2v.finalize()
+    h = run_gpu(w2v, ids, V, D, window, K, 0.025, 1e-3, 5, L, mode=0, opts={"tma_gather": 1})
+    assert h["stats"]["row_touches"] == o_st["row_touches"] and np.isfinite(h["M_in"]).all()
