@@ -96,8 +96,8 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          between iterations"): all SMs, every row access waits on a per-row
  *                          ticket taken in corpus order — bit-identical to mode 1 (rows kernel,
  *                          2*window+K+1 <= 32; a chunk's ticket table, sentence_len x
- *                          (2*window+K+1) u32, lives in shared memory: EINVAL when it and the
- *                          slab exceed 227 KB, e.g. sentence_len 4096 with 2*window+K+1 > 13)
+ *                          (2*window+K+1) u32, lives in shared memory, or in global memory when
+ *                          it does not fit beside the slab)
  *  "sentence_len"          chunk length L of C5 (1..4096; default 1000)
  *  "sync_period_words"     P of C13 (>=1; default 2^20)
  *  "sync_hot_rows"         C14: rows [0,H) of both matrices (the Zipf-hot prefix)

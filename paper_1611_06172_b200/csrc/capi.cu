@@ -141,6 +141,8 @@ struct Ctx {
     unsigned long long* chunk_ctr = nullptr;
     int64_t* dp_tmp = nullptr;
     uint32_t* tick = nullptr;               // mode 2: [issue 2V | done 2V] ticket counters
+    uint32_t* tick_tab = nullptr;           // mode 2: per-CTA ticket tables in global memory
+    size_t tick_tab_cap = 0;
     unsigned long long* turn = nullptr;     // mode 2: chunk turn of the current launch
     // batch stream of one launch range (batch.cu -> step kernels), capacity in chunks
     // two sets: the batch kernel fills set (j+1)&1 on the side stream while the step kernel
@@ -661,14 +663,18 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         return bail(fail(W2V_EINVAL, "w2v_train: Alg.1 kernel does not cover D=%d, K=%d", g.D, g.K));
     // kernel choice: 1 per-target rows, 2 window-resident (one warp per unit),
     // 3 window-resident warp-specialised (a CTA of column warps + an IO warp per unit)
+    const size_t kSmemMax = 227 * 1024;
     int32_t off_win = 0, off_row = 0, off_wg = 0;
     const size_t wb_win = win_warp_bytes(g.L, g.window, g.K, g.D, &off_win);
     int32_t off_tick = 0;
-    const size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row, g.mode == 2 ? &off_tick : nullptr);
+    size_t wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row, g.mode == 2 ? &off_tick : nullptr);
+    if (g.mode == 2 && wb_row > kSmemMax) {  // the ticket table goes to global memory instead
+        wb_row = step_warp_bytes(g.L, g.window, g.K, g.D, &off_row, nullptr);
+        off_tick = -1;
+    }
     const size_t wb_wg = wg_cta_bytes(g.L, g.window, g.K, g.D, &off_wg);
     int32_t off_ring = 0;
     const size_t wb_ring = ring_warp_bytes(g.L, g.window, g.K, g.D, &off_ring);
-    const size_t kSmemMax = 227 * 1024;
     int kern = g.kernel == 0 ? 1 : g.kernel;
     if (g.algorithm == 1) kern = 0;  // alg1.cu
     if (g.mode == 2) {  // NEXT-4: the rows kernel with per-row tickets (hogbatch.cu)
@@ -715,6 +721,18 @@ int w2v_train(const int32_t* ids_in, int64_t n, int32_t epochs) {
         if (g.ctas_per_sm > 0 && g.ctas_per_sm < occ) occ = g.ctas_per_sm;
         ctas = g.sms * occ;
     }
+    if (g.mode == 2 && off_tick < 0) {  // global ticket tables, one per CTA of this launch grid
+        const size_t need = (size_t)ctas * ((g.L + 3) & ~3) * (2 * g.window + g.K + 1);
+        if (need > g.tick_tab_cap) {
+            cudaFree(g.tick_tab);
+            g.tick_tab = nullptr;
+            g.tick_tab_cap = 0;
+            int rc = dmalloc((void**)&g.tick_tab, need * sizeof(uint32_t), "mode-2 ticket tables");
+            if (rc) return bail(rc);
+            g.tick_tab_cap = need;
+        }
+    }
+    p.tick_glob = g.tick_tab;
     g.st.units_per_sm = kern == 4 ? ring_units : ctas >= g.sms ? ctas / g.sms : 1;
     // stats: 1 rows, 2 window, 3 window warp-specialised, 4 alg1, 5 ring
     g.st.kernel = kern == 0 ? 4 : kern == 4 ? 5 : kern;
@@ -1130,7 +1148,7 @@ int w2v_finalize(void) {
     cudaFree(g.ds_owned);
     cudaFree(g.corpus); cudaFree(g.counts); cudaFree(g.thr); cudaFree(g.P); cudaFree(g.scratch);
     cudaFree(g.G); cudaFree(g.info); cudaFree(g.dstats); cudaFree(g.chunk_ctr); cudaFree(g.dp_tmp);
-    cudaFree(g.tick); cudaFree(g.turn);
+    cudaFree(g.tick); cudaFree(g.turn); cudaFree(g.tick_tab);
     cudaStreamSynchronize(g.side);
     cudaStreamSynchronize(g.comm_stream);
     cudaStreamSynchronize(g.copy_stream);

@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(32, W2V_MINB) hogbatch_step_kernel(const StepP
         W2V_T(ph[0] += clock64() - t0;)
         const int nk = *nk_s;
         if (lane == 0) st_words += (unsigned long long)cnt;
-        uint32_t* tick = reinterpret_cast<uint32_t*>(wbase + p.tick_off);  // [nk][RMAX] (mode 2)
+        uint32_t* tick = p.tick_off >= 0 ? reinterpret_cast<uint32_t*>(wbase + p.tick_off)  // [nk][RMAX] (mode 2)
+                                         : p.tick_glob + (size_t)blockIdx.x * p.Lp * RMAX;
         if (ticketed) {
             // NEXT-4 (dependences between iterations): chunks take their turn in
             // corpus order; during its turn a chunk takes one ticket per row access of each of

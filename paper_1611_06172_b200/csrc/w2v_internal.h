@@ -72,7 +72,9 @@ struct StepParams {
     uint32_t* tick_issue;
     uint32_t* tick_done;
     unsigned long long* turn;
-    int32_t tick_off;
+    int32_t tick_off;     // >= 0: byte offset of the table in the warp's smem; -1: in tick_glob
+    uint32_t* tick_glob;  // mode 2 ticket tables in global memory, [CTA][Lp][2w+K+1], when the
+                          // table does not fit beside the slab (long chunks x many rows)
     int32_t scatter_wait; // 1: a target waits for its reductions to complete before the next
                           // target's gathers (R11); 0 (Hogwild only): until they are read
     int32_t ring_delta;   // ring kernel, deterministic mode: 1 = write back slot - original

@@ -84,13 +84,8 @@ def test_random_shape_parity(w2v, case):  # noqa: F811
     R = 2 * window + K + 1
     if R <= 32:
         w2v.finalize()
-        # mode 2 keeps a chunk's ticket table [L][R] u32 in shared memory: long chunks with many
-        # rows per target do not fit and are refused (EINVAL), never run wrongly
-        if ((L + 3) & ~3) * R * 4 > 200 * 1024:
-            with pytest.raises(w2v.W2VError, match="shared memory"):
-                run_gpu(w2v, ids, V, D, window, K, alpha, t, seed, L, epochs=c["epochs"], mode=2,
-                        opts={"allow_target_negative": c["allow"], "kernel": 1})
-            return
+        # (a chunk's ticket table [L][R] u32 lives in shared memory, or in global memory when it
+        # does not fit beside the slab: long chunks x many rows per target)
         g2 = run_gpu(w2v, ids, V, D, window, K, alpha, t, seed, L, epochs=c["epochs"], mode=2,
                      opts={"allow_target_negative": c["allow"], "kernel": 1})
         assert np.array_equal(g2["M_in"], results[1]["M_in"]) and np.array_equal(g2["M_out"], results[1]["M_out"]), tag
