@@ -65,7 +65,10 @@ def main():
         st = run(ids, cfg, opts)
         print("ok", cfg.idx, opts, st["targets"], flush=True)
     for opts in ({"sync_period_words": 1000}, {"sync_period_words": 1000, "sync_hot_rows": 100, "sync_cold_every": 2,
-                                                "sync_overlap": 1}):
+                                                "sync_overlap": 1},
+                 {"sync_period_words": 1000, "sync_device": 1},
+                 {"sync_period_words": 1000, "sync_hot_rows": 100, "sync_cold_every": 2, "sync_overlap": 1,
+                  "sync_device": 1}):
         st = run(ids1, c1, dict(opts, mode=1), dp=True)
         print("ok dp", opts, st["syncs"], st["syncs_hot"], flush=True)
     print("sanitize_run done")
