@@ -1,4 +1,5 @@
-"""Hogwild at the FULL headline size against the sequential algorithm (opt-in: W2V_FULLSIZE=1).
+"""Hogwild at FULL size against the sequential algorithm (opt-in: W2V_FULLSIZE=1; select configs
+with W2V_FULLSIZE_CONFIGS=3,4). cfg4 (D = 128, K = 15, window 8) runs the TMA gather4 path.
 
 cfg3 (V = 1M, D = 300, window 5, K = 5, t = 1e-4, 800M planted-Zipf tokens), one epoch:
   * Hogwild: the bench's launch configuration (all SMs, the default rows kernel; and the ring);
@@ -42,8 +43,12 @@ def _train(w2v, dev, cfg, mode, kernel, tail_from):  # noqa: F811
     return st, M_in, M_out
 
 
-def test_cfg3_fullsize_hogwild_vs_sequential(w2v):  # noqa: F811
-    cfg = inputs.CONFIGS[3]
+@pytest.mark.parametrize("config", [3, 4])
+def test_cfg3_fullsize_hogwild_vs_sequential(w2v, config):  # noqa: F811
+    """cfg3 (the headline) and cfg4 (D = 128, K = 15, window 8: the TMA gather4 path)."""
+    if os.environ.get("W2V_FULLSIZE_CONFIGS") and str(config) not in os.environ["W2V_FULLSIZE_CONFIGS"].split(","):
+        pytest.skip("not selected in W2V_FULLSIZE_CONFIGS")
+    cfg = inputs.CONFIGS[config]
     dev = torch.empty(cfg.n, dtype=torch.int32, device="cuda")
     cfg.corpus().tokens_cuda(0, cfg.n, dev)
     tail_from = (cfg.n * 9 // 10) // cfg.L * cfg.L
@@ -54,7 +59,7 @@ def test_cfg3_fullsize_hogwild_vs_sequential(w2v):  # noqa: F811
         whole = st["loss_sum"] / st["loss_pairs"]
         held = heldout_loss(M_in, M_out, cfg, cfg.n, 200_000)
         res[name] = (whole, tail, held, st["row_touches"], st["ms_total"])
-        print(f"cfg3 full {name}: loss/pair whole {whole:.6f}, final 10% {tail:.6f}, held-out {held:.6f}; "
+        print(f"cfg{config} full {name}: loss/pair whole {whole:.6f}, final 10% {tail:.6f}, held-out {held:.6f}; "
               f"row_touches {st['row_touches']}, {st['ms_total'] / 1e3:.1f} s")
     seq = res["sequential (mode 1)"]
     for name in ("hogwild rows", "hogwild ring"):
