@@ -148,7 +148,10 @@ int w2v_init(int64_t V, int32_t D, int32_t window, int32_t K, float alpha, float
  *                          2 window-resident rows (hogbatch_win.cu; window <= 15), 3 window-
  *                          resident warp-specialised (hogbatch_wg.cu; window <= 15), 4 window
  *                          ring with the originals in tensor memory (hogbatch_ring.cu; window
- *                          <= 15): ~1 gather + 1 reduction per kept position for M_in
+ *                          <= 15): ~1 gather + 1 reduction per kept position for M_in. In
+ *                          Hogwild mode a slot holds a row for 2*window+1 targets, so with
+ *                          long windows the deltas of stale Zipf-hot rows overshoot (cfg4,
+ *                          window 8: final loss +2.6%); exact in modes 1/2
  *  "ring_writeback"        kernel 4 in deterministic mode: 0 (default) stores the slot value
  *                          (the exact sequential row), 1 reduces slot - original as Hogwild does
  *  "check_finite"          1 (default): scan the model for NaN/Inf after every w2v_train (one
