@@ -237,11 +237,16 @@ def measure_caps(row_bytes, rows_per_target, units_per_sm):
         return None
     lib = ctypes.CDLL(PEAKS_SO)
     d = ctypes.c_double(0.0)
-    caps = {}
+    mhz = ctypes.c_double(0.0)
+    caps, clk = {}, {}
     for w in sorted({units_per_sm, 8, 12, 16}):
-        if lib.peaks_l2_rowpath(int(row_bytes), int(rows_per_target), int(w), ctypes.byref(d)) == 0:
-            caps[w] = d.value
-    out = {"l2_rowpath_gbs": max(caps.values()) if caps else None, "l2_rowpath_by_units": caps}
+        if lib.peaks_l2_rowpath_clk(int(row_bytes), int(rows_per_target), int(w), 0, ctypes.byref(d),
+                                    ctypes.byref(mhz)) == 0:
+            caps[w], clk[w] = d.value, mhz.value
+    best = max(caps, key=caps.get) if caps else None
+    # the SM clock each cap run ran at (clock64 over its event time)
+    out = {"l2_rowpath_gbs": caps[best] if caps else None, "l2_rowpath_by_units": caps,
+           "l2_rowpath_sm_mhz": clk.get(best), "l2_rowpath_sm_mhz_by_units": clk}
     if lib.peaks_ffma2(ctypes.byref(d)) == 0:
         out["ffma2_tflops"] = d.value
     if lib.peaks_l2_read(ctypes.byref(d)) == 0:
@@ -398,6 +403,7 @@ def run_ours(args):
             "gpu_launches": int(sum(s["launches"] for s in steps)),
             "clocks": clk.summary(),
         }
+        clk_summary = out["clocks"]
         l2cap = caps and caps.get("l2_rowpath_gbs")
         if l2cap:
             out["roofline"] = {
@@ -414,6 +420,11 @@ def run_ours(args):
                 "moved_frac": last["bytes_moved"] / kern_s / 1e9 / l2cap,
                 "algorithmic_bytes_per_launch": last["bytes_row"] / max(last["step_launches"], 1),
                 "kernel_ms_per_step": kern_max, "kernel_share_of_step": kern_max / (ms_max / args.steps)}
+            # context: the SM clock the best cap run ran at (clock64 over its event time) beside
+            # the timed region's (clocks.sm_mhz); the cap's bytes/s barely move with the SM clock
+            # (L2 has its own), the kernel's follow it (its issue/latency side), r02_ablations §19
+            out["roofline"]["cap_sm_mhz"] = caps.get("l2_rowpath_sm_mhz")
+            out["roofline"]["run_sm_mhz"] = (clk_summary or {}).get("sm_mhz")
         else:  # tools lib missing: report against HBM only
             out["roofline"] = {"bound": "hbm", "achieved": bps / 1e9, "peak": peak, "unit": "GB/s",
                                "frac": bps / 1e9 / peak, "traffic": traffic}

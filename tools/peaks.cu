@@ -15,6 +15,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Xcompiler -fPIC -shared -o tools/libw2v_peaks.so tools/peaks.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -31,7 +32,8 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 // one warp = one unit: batches of R rows gathered then reduced, like one target of the step
 // (rows [0, n_store) of a batch are written back by a plain bulk store instead of the reduction)
 __global__ void rowpath_kernel(float* base, uint32_t nrows, uint32_t row_floats, uint32_t row_bytes, int R,
-                               int batches, int warp_bytes, int n_store) {
+                               int batches, int warp_bytes, int n_store, unsigned long long* clk) {
+    if (clk && blockIdx.x == 0 && threadIdx.x == 0) clk[0] = clock64();   // SM cycles over the run
     extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* wb = smem + (size_t)w * warp_bytes;
@@ -78,6 +80,7 @@ __global__ void rowpath_kernel(float* base, uint32_t nrows, uint32_t row_floats,
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         __syncwarp();
     }
+    if (clk && blockIdx.x == 0 && threadIdx.x == 0) clk[1] = clock64();
 }
 
 __global__ void ffma2_kernel(float* out, int iters) {
@@ -262,14 +265,18 @@ extern "C" {
 
 // row_bytes % 16 == 0; R rows per batch (<= 32); warps_per_sm resident 1-warp... units per SM.
 // Returns 0 and *gbs = (gathered + reduced row bytes) / s, or a CUDA error code.
-int peaks_l2_rowpath_store(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs);
+int peaks_l2_rowpath_clk(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs, double* mhz);
+int peaks_l2_rowpath_store(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs) {
+    return peaks_l2_rowpath_clk(row_bytes, R, warps_per_sm, n_store, gbs, nullptr);
+}
 int peaks_l2_rowpath(int row_bytes, int R, int warps_per_sm, double* gbs) {
-    return peaks_l2_rowpath_store(row_bytes, R, warps_per_sm, 0, gbs);
+    return peaks_l2_rowpath_clk(row_bytes, R, warps_per_sm, 0, gbs, nullptr);
 }
 
 // the same with the first n_store rows of every batch written back by a plain bulk store
-// (cp.async.bulk.global.shared::cta) instead of the fp32 reduce-add
-int peaks_l2_rowpath_store(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs) {
+// (cp.async.bulk.global.shared::cta) instead of the fp32 reduce-add; *mhz (if given) = the SM
+// clock the timed run ran at (block 0's clock64 span over the launch's CUDA-event time)
+int peaks_l2_rowpath_clk(int row_bytes, int R, int warps_per_sm, int n_store, double* gbs, double* mhz) {
     if (row_bytes <= 0 || row_bytes % 16 || R < 1 || R > 32 || warps_per_sm < 1) return -1;
     const int sms = sm_count();
     const uint32_t row_floats = (uint32_t)((row_bytes + 127) / 128 * 32);   // 128-B row stride
@@ -282,21 +289,28 @@ int peaks_l2_rowpath_store(int row_bytes, int R, int warps_per_sm, int n_store, 
     while (wpc > 8) { wpc = (wpc + 1) / 2; cpsm *= 2; }
     const int smem = wpc * warp_bytes;
     cudaFuncSetAttribute(rowpath_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int batches = 2000;
+    const char* nb = getenv("W2V_CAP_BATCHES");
+    const int batches = nb ? atoi(nb) : 2000;
+    unsigned long long* clk = nullptr;
+    cudaMalloc(&clk, 16);
     Timer t;
     float ms = 0.f;
     for (int pass = 0; pass < 2; ++pass) {
         cudaEventRecord(t.a);
         rowpath_kernel<<<sms * cpsm, 32 * wpc, smem>>>(base, nrows, row_floats, (uint32_t)row_bytes, R, batches,
-                                                       warp_bytes, n_store);
+                                                       warp_bytes, n_store, clk);
         cudaEventRecord(t.b);
         cudaEventSynchronize(t.b);
         cudaEventElapsedTime(&ms, t.a, t.b);
     }
+    unsigned long long hc[2] = {0, 0};
+    cudaMemcpy(hc, clk, 16, cudaMemcpyDeviceToHost);
+    cudaFree(clk);
     const cudaError_t e = cudaGetLastError();
     cudaFree(base);
     if (e != cudaSuccess) return (int)e;
     *gbs = (double)sms * cpsm * wpc * batches * R * row_bytes * 2.0 / (ms * 1e-3) / 1e9;
+    if (mhz) *mhz = hc[1] > hc[0] ? (double)(hc[1] - hc[0]) / (ms * 1e3) : 0.0;
     return 0;
 }
 
