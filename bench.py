@@ -101,7 +101,7 @@ class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, gpu):
         self.gpu, self.rows, self.proc = gpu, [], None
@@ -136,8 +136,16 @@ class Clocks:
         mx = [float(r[2]) for r in self.rows if len(r) > 7 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows if len(r) > 7 for i in range(4) if r[4 + i] == "Active"})
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        pw = [num(r[8]) for r in self.rows if len(r) > 9 and num(r[8]) is not None]
+        lim = [num(r[9]) for r in self.rows if len(r) > 9 and num(r[9]) is not None]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w": float(np.median(pw)) if pw else None, "power_limit_w": max(lim) if lim else None}
 
 
 def host_threads() -> int:
